@@ -1,0 +1,252 @@
+/*
+ * la.h — C ABI of the KV-buffered Gated DeltaNet decode library (labuf).
+ *
+ * Implements the IO-aware serving mechanism of arxiv 2605.19049 for Gated
+ * DeltaNet (GDN) linear attention on NVIDIA B200 (sm_100a).  Citations
+ * "P:n" are lines of the paper text; "Eq. k" counts its numbered
+ * display equations in order; "Zk" are the readings listed in DESIGN.md.
+ *
+ * ---------------------------------------------------------------- math
+ * Per request slot r and V head h (QK head floor(h*Hk/Hv)), with column
+ * vectors and the state S in R^{d_v x d_k} (the transpose of the paper's
+ * row-vector S, reading Z1), the method reaches exactly (up to rounding) the
+ * GDN recurrence:
+ *     S_t = alpha_t S_{t-1} (I - beta_t k_t k_t^T) + beta_t v_t k_t^T,
+ *     o_t = S_t q_t.
+ * It keeps, per slot and head, a KV buffer of records (k_i, u_i, G_i), where
+ *     u_i = beta_i (v_i - e^{G_i} S0 k_i - sum_{l<i} e^{G_i-G_l} (k_i.k_l) u_l)
+ * is the delta value and G_i the cumulative log decay
+ * since the last fold (reading Z2).  Outputs are computed from one read of
+ * S0 plus the buffer, and the buffer is folded into the state in
+ * batch:  S <- e^{G_last} S0 + sum_i e^{G_last - G_i} u_i k_i^T.
+ *
+ * ---------------------------------------------------------------- layout
+ * Device memory is caller-owned (allocate it with torch.empty or cudaMalloc;
+ * sizes from la_buf_query).  All pointers are DEVICE pointers unless noted.
+ *   state   fp32 [R][Hv][d_v][d_k]   (d_k contiguous; 64 KiB per (slot,head))
+ *   buffer  one allocation holding, at offsets reported by la_buf_query:
+ *           K [R][Hk][T][d_k] in_dtype, U [R][Hv][T][d_v] u_dtype,
+ *           G [R][Hv][T] fp32, and when keep_raw: V [R][Hv][T][d_v] in_dtype,
+ *           B [R][Hv][T] fp32;   T = max(chunk + max_drafts, short_cap)
+ *   meta    int32 occ[R], len[R], mode[R], ticket[R], then uint32 status
+ * Per-call tensors (row-major, batch = contiguous slot range [first, first+n)):
+ *   q, k  [n][n_tok][Hk][d_k] in_dtype;  v [n][n_tok][Hv][d_v] in_dtype;
+ *   alpha, beta fp32 [n][n_tok][Hv];   o fp32 [n][n_tok][Hv][d_v]
+ *   (n_tok = 1 for decode / recurrent step, n_draft for verify, n_new for
+ *   direct, n_tok for prefill).  Inputs must be 16-byte aligned.
+ *
+ * ---------------------------------------------------------------- contract
+ * Streams: every call enqueues asynchronously on `stream` (a cudaStream_t;
+ *   NULL = legacy default stream) and never synchronises, except
+ *   la_device_status.  Calls on one handle must be stream-ordered and issued
+ *   from one host thread at a time.
+ * Errors: every function returns la_status.  On any return other than LA_OK
+ *   nothing was enqueued and the host occupancy mirror is unchanged
+ *   (all-or-nothing); la_last_error() returns a thread-local message.
+ * Occupancy: the library keeps an exact host mirror of occ/len/mode per slot;
+ *   it advances deterministically (decode +1, flush/commit -> 0, direct +n_new,
+ *   prefill -> 0) and never needs device values.  Device copies in `meta`
+ *   are what the kernels read, so whole cycles can be captured in CUDA graphs;
+ *   a replayed graph must cover closed cycles (the mirror does not see
+ *   replays).
+ * Determinism: identical inputs give bit-identical outputs (no float atomics).
+ */
+#ifndef LABUF_LA_H
+#define LABUF_LA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define LA_API __attribute__((visibility("default")))
+#else
+#define LA_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct la_buf la_buf;   /* opaque host handle; owns NO device memory */
+typedef void *la_stream;        /* cudaStream_t */
+
+typedef enum {
+    LA_OK = 0,
+    LA_ERR_INVALID = 1,      /* null/misaligned pointer, bad range or count   */
+    LA_ERR_UNSUPPORTED = 2,  /* d != 128, Hv % Hk != 0, unsupported dtype mix  */
+    LA_ERR_CAPACITY = 3,     /* buffer would overflow (forgot la_flush, ...)   */
+    LA_ERR_MODE = 4,         /* wrong slot mode / pending verify / no verify   */
+    LA_ERR_CUDA = 5,         /* CUDA launch or runtime error                  */
+    LA_ERR_NCCL = 6          /* NCCL error (tensor-parallel helpers)          */
+} la_status;
+
+typedef enum { LA_DT_F32 = 0, LA_DT_BF16 = 1, LA_DT_F16 = 2 } la_dtype;
+typedef enum { LA_MODE_CHUNKWISE = 0, LA_MODE_DIRECT = 1 } la_mode;
+typedef enum {
+    LA_FLUSH_FULL = 0,   /* fold only slots whose buffer holds `chunk` records */
+    LA_FLUSH_FORCE = 1   /* fold every non-empty slot; a DIRECT slot is compressed
+                            into a fresh state and switches to CHUNKWISE */
+} la_flush_kind;
+
+/* Device status bits (la_device_status), set only when config.validate = 1. */
+#define LA_STATUS_BAD_ALPHA   0x1u  /* alpha not in (0, 1]  (reading Z9)      */
+#define LA_STATUS_BAD_BETA    0x2u  /* beta not in [0, 1]                      */
+#define LA_STATUS_NONFINITE   0x4u  /* non-finite q/k/v                         */
+#define LA_STATUS_BAD_NACC    0x8u  /* n_accepted outside [0, n_draft] (clamped) */
+
+typedef struct {
+    int32_t max_slots;   /* R >= 1                                            */
+    int32_t n_qk_heads;  /* Hk >= 1                                           */
+    int32_t n_v_heads;   /* Hv, Hv % Hk == 0, Hv/Hk in {1,2,4}                */
+    int32_t d_k, d_v;    /* must be 128                               */
+    int32_t chunk;       /* buffer size C in [1, 64] (best near 2 sqrt d) */
+    int32_t max_drafts;  /* N_max in [0, 16]                                  */
+    int32_t short_cap;   /* direct-mode capacity in [0, 128] (<= d)     */
+    int32_t in_dtype;    /* la_dtype of q,k,v: LA_DT_BF16 or LA_DT_F32        */
+    int32_t u_dtype;     /* la_dtype of buffered u: F32, or F16 with BF16 in  */
+    int32_t keep_raw;    /* 1: also store v and beta per record               */
+    int32_t validate;    /* 1: device-side value checks -> status word        */
+} la_config;
+
+typedef struct {
+    size_t state_bytes;  /* fp32 [R][Hv][d_v][d_k]                            */
+    size_t buffer_bytes; /* K, U, G [, V, B] records                          */
+    size_t meta_bytes;   /* int32 occ, len, mode, ticket [R] + uint32 status  */
+    size_t align;        /* required base alignment of all three (1024)       */
+    int32_t capacity;    /* T, records per (slot, head)                       */
+    size_t off_k, off_u, off_g, off_v, off_b;   /* offsets inside `buffer`    */
+    size_t record_bytes; /* bytes per record per slot-layer (all heads)       */
+} la_sizes;
+
+/* Sizing query; no device access.  LA_ERR_INVALID/UNSUPPORTED on bad config. */
+LA_API la_status la_buf_query(const la_config *cfg, la_sizes *out);
+
+/* Create a handle over caller-owned device memory.  `state`, `buffer`, `meta`
+ * must be `align`-aligned device pointers of at least the queried sizes and
+ * outlive the handle.  Does not initialise device memory: call
+ * la_request_reset on every slot before use.  `device` is the CUDA ordinal. */
+LA_API la_status la_buf_create(const la_config *cfg, void *state, void *buffer, void *meta,
+                        int32_t device, la_buf **out);
+LA_API la_status la_buf_destroy(la_buf *buf);   /* frees host memory only */
+
+/* Reset slots [first, first+n): occ = len = 0, mode as given, and (if
+ * zero_state) the state set to 0.  Clears a pending verify. */
+LA_API la_status la_request_reset(la_buf *buf, int32_t first, int32_t n, int32_t mode,
+                           int32_t zero_state, la_stream stream);
+
+/* Buffered decode step, kernel (1).  For each slot in the
+ * range (CHUNKWISE, occ < chunk, no pending verify): computes u_t and
+ * o_t = e^{G_t} S0 q_t + sum_i e^{G_t-G_i} (q_t.k_i) u_i + (q_t.k_t) u_t from
+ * one read of the state, appends (k_t, u_t, G_t) at position occ, occ += 1.
+ * Does not fold: call la_flush(LA_FLUSH_FULL) after the step that fills the
+ * buffer.  LA_ERR_CAPACITY if some slot has occ == chunk. */
+LA_API la_status la_decode_step(la_buf *buf, int32_t first, int32_t n, const void *q,
+                         const void *k, const void *v, const float *alpha,
+                         const float *beta, float *o, la_stream stream);
+
+/* Flush, kernel (2): S <- e^{G_last} S0 +
+ * sum_{i<occ} e^{G_last-G_i} u_i k_i^T on the 5th-gen tensor cores
+ * (tcgen05, split-TF32, accumulator in TMEM), occ <- 0.  FULL folds slots
+ * with occ == chunk, FORCE every non-empty slot (DIRECT slots: compression
+ * with S0 = 0, mode -> CHUNKWISE).  A range with nothing to fold is a no-op
+ * (not an error). */
+LA_API la_status la_flush(la_buf *buf, int32_t first, int32_t n, int32_t kind, la_stream stream);
+
+/* Parallel draft verification, kernel (3): outputs of
+ * n_draft drafts per slot from one read of the state, the buffered records
+ * and the drafts themselves (n_draft x n_draft forward substitution).  Draft
+ * records are written at positions occ .. occ+n_draft-1 but occ does not move
+ * and no temporary state exists.  Requires 1 <= n_draft <= max_drafts,
+ * occ + n_draft <= T, no pending verify.  Marks the range pending. */
+LA_API la_status la_verify_drafts(la_buf *buf, int32_t first, int32_t n, int32_t n_draft,
+                           const void *q, const void *k, const void *v,
+                           const float *alpha, const float *beta, float *o,
+                           la_stream stream);
+
+/* Accepted-prefix commit (Eq. 8): folds records
+ * [0, occ + n_accepted[r]) into the state (kernel (2)), occ <- 0.
+ * n_accepted: DEVICE int32 [n], clamped to [0, n_draft] (status bit when
+ * validate=1).  occ + n_accepted = 0 leaves the state bit-identical.
+ * LA_ERR_MODE unless every slot in the range has a pending verify of the
+ * same n_draft. */
+LA_API la_status la_commit_accepted(la_buf *buf, int32_t first, int32_t n,
+                             const int32_t *n_accepted, la_stream stream);
+
+/* Direct (KV-only) short-context decoding, kernel (4) (P:200-213,
+ * P:374-378): for DIRECT slots, outputs of n_new new tokens computed only
+ * from the buffered records of the whole context and the new tokens
+ * (n_new x n_new forward substitution); no state is read or written.
+ * Appends the records, len += n_new.  n_new = 1 is a decode step, n_new = P
+ * a short prefill.  LA_ERR_CAPACITY if len + n_new > short_cap. */
+LA_API la_status la_direct_short(la_buf *buf, int32_t first, int32_t n, int32_t n_new,
+                          const void *q, const void *k, const void *v,
+                          const float *alpha, const float *beta, float *o,
+                          la_stream stream);
+
+/* Chunkwise prefill: folds a prompt of n_tok tokens into the state
+ * of CHUNKWISE slots with occ == 0, in chunks of `chunk` tokens: each chunk
+ * runs the forward-substitution kernel (the UT transform of P:395-397) and
+ * the tensor-core fold.  o may be NULL; otherwise it receives the
+ * prompt outputs [n][n_tok][Hv][d_v].  Leaves occ = 0. */
+LA_API la_status la_prefill(la_buf *buf, int32_t first, int32_t n, int32_t n_tok,
+                     const void *q, const void *k, const void *v,
+                     const float *alpha, const float *beta, float *o,
+                     la_stream stream);
+
+/* Conventional recurrent decode, kernel (5a) (Table 2):
+ * reads and writes the whole state every token.  In-run IO baseline.
+ * Requires CHUNKWISE slots with occ == 0. */
+LA_API la_status la_recurrent_step(la_buf *buf, int32_t first, int32_t n, const void *q,
+                            const void *k, const void *v, const float *alpha,
+                            const float *beta, float *o, la_stream stream);
+
+/* Conventional recurrent speculative verification, kernel (5b) (P:94,
+ * P:183): reads S once, takes n_draft sequential steps and writes one
+ * temporary state per draft: temp fp32 [n][n_draft][Hv][d_v][d_k]. */
+LA_API la_status la_recurrent_verify(la_buf *buf, int32_t first, int32_t n, int32_t n_draft,
+                              const void *q, const void *k, const void *v,
+                              const float *alpha, const float *beta, float *temp,
+                              float *o, la_stream stream);
+
+/* Baseline commit: the slot's state is replaced by the temporary state of the
+ * last accepted draft (Fig. 3); n_accepted = 0 leaves it unchanged. */
+LA_API la_status la_recurrent_commit(la_buf *buf, int32_t first, int32_t n, int32_t n_draft,
+                              const int32_t *n_accepted, const float *temp,
+                              la_stream stream);
+
+/* Canonical state export/import of one slot: fp32 [Hv][d_v][d_k], device
+ * pointers, async on `stream`. */
+LA_API la_status la_state_get(la_buf *buf, int32_t slot, float *dst, la_stream stream);
+LA_API la_status la_state_set(la_buf *buf, int32_t slot, const float *src, la_stream stream);
+
+/* Host mirror of one slot (no device access). */
+LA_API la_status la_slot_info(la_buf *buf, int32_t slot, int32_t *occ, int32_t *len,
+                       int32_t *mode, int32_t *pending_drafts);
+
+/* Synchronises `stream`, returns the device status word in *flags, and
+ * copies the device occ/len/mode of all slots into the optional host arrays
+ * (each int32[R], may be NULL). */
+LA_API la_status la_device_status(la_buf *buf, la_stream stream, uint32_t *flags,
+                           int32_t *occ_host, int32_t *len_host, int32_t *mode_host);
+
+/* Number of kernels this handle has launched since creation (all la_* calls). */
+LA_API int64_t la_kernel_launches(const la_buf *buf);
+
+/* Thread-local message of the last non-LA_OK return on this thread. */
+LA_API const char *la_last_error(void);
+
+/* ----------------------------------------------- tensor-parallel helpers
+ * Heads are partitioned over ranks (each handle created with Hk/G, Hv/G);
+ * head outputs are gathered with one NCCL all-gather per layer (DESIGN.md
+ * "Multi-GPU").  The only collective in the library. */
+LA_API la_status la_tp_unique_id(void *id_out /* 128 bytes, host */);
+LA_API la_status la_tp_init(const void *unique_id /* 128 bytes, host */, int32_t rank,
+                     int32_t world, int32_t device, void **comm_out);
+LA_API la_status la_tp_allgather(void *comm, const void *send, void *recv,
+                          size_t bytes_per_rank, la_stream stream);
+LA_API la_status la_tp_destroy(void *comm);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LABUF_LA_H */

@@ -1,0 +1,60 @@
+"""Build liblabuf.so in-tree with nvcc for sm_100a (no JIT, no torch extension).
+
+    python -m paper_2605_19049_b200.build [--force]
+
+The shared library exports exactly the C ABI of include/la.h.  The CUDA
+runtime is linked statically; NCCL is dlopen'ed at run time (csrc/tp.cpp).
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+LIB = os.path.join(PKG, "liblabuf.so")
+NCCL_INC = "/opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/nccl/include"
+
+CU_SOURCES = ["chunk.cu", "fold.cu", "recurrent.cu"]
+CPP_SOURCES = ["la.cpp", "tp.cpp"]
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def _sources():
+    return [os.path.join(CSRC, f) for f in CU_SOURCES + CPP_SOURCES]
+
+
+def _deps():
+    out = _sources() + [os.path.join(CSRC, f) for f in ("device.cuh", "internal.h")]
+    out.append(os.path.join(ROOT, "include", "la.h"))
+    return out
+
+
+def needs_build() -> bool:
+    if not os.path.exists(LIB):
+        return True
+    t = os.path.getmtime(LIB)
+    return any(os.path.getmtime(p) > t for p in _deps())
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    if not force and not needs_build():
+        return LIB
+    nvcc = os.environ.get("NVCC", "nvcc")
+    cmd = [nvcc, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+           "-Xcompiler", "-fvisibility=hidden", "-shared", "-o", LIB + ".tmp",
+           f"-I{os.path.join(ROOT, 'include')}", f"-I{NCCL_INC}",
+           "-Xptxas", "-warn-spills", "--expt-relaxed-constexpr",
+           *_sources(), "-ldl", "-lpthread"]
+    if verbose:
+        cmd.insert(1, "-Xptxas=-v")
+    subprocess.check_call(cmd)
+    os.replace(LIB + ".tmp", LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
+    print(LIB)

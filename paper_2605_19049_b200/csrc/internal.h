@@ -1,0 +1,89 @@
+// internal.h — kernel argument blocks and launcher declarations shared by the
+// host library (la.cpp) and the kernels (*.cu).  Internal; not the C ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace labuf {
+
+constexpr int kD = 128;          // d_k = d_v
+constexpr int kRows = 32;        // d_v rows per V head per chunk-kernel CTA
+constexpr int kMaxNewPerLaunch = 16;
+
+enum DType : int { DT_F32 = 0, DT_BF16 = 1, DT_F16 = 2 };
+
+struct Dims {
+    int R, Hk, Hv, g, T, C;
+    int in_dt, u_dt, keep_raw, validate;
+};
+
+struct Ptrs {
+    float *state;            // [R][Hv][d][d]
+    void *K;                 // [R][Hk][T][d] in_dt
+    void *U;                 // [R][Hv][T][d] u_dt
+    float *G;                // [R][Hv][T]
+    void *V;                 // [R][Hv][T][d] in_dt (keep_raw)
+    float *B;                // [R][Hv][T]        (keep_raw)
+    int *occ, *len, *mode, *ticket;
+    unsigned *status;
+};
+
+// What the chunk-attend kernel does with the counters and the state.
+enum ChunkKind : int {
+    CK_DECODE = 0,   // state, append at occ, occ += n_new           (kernel 1)
+    CK_VERIFY = 1,   // state, write drafts at occ.., occ unchanged  (kernel 3)
+    CK_DIRECT = 2,   // no state, append at len, len += n_new        (kernel 4)
+    CK_PREFILL = 3,  // state, append at occ, occ += n_new (then fold)
+};
+
+struct ChunkArgs {
+    Dims dm;
+    Ptrs p;
+    int first, n;       // slot range
+    int n_new;          // tokens processed per slot in this launch (<= kMaxNewPerLaunch)
+    int j0_cap;         // max over the range of the buffered count j0 (sizes smem)
+    int tok_total;      // tokens per slot in the caller's q/k/v/alpha/beta/o arrays
+    int tok_offset;     // first token of this launch inside those arrays
+    int kind;
+    const void *q, *k, *v;
+    const float *alpha, *beta;
+    float *o;           // may be null (prefill without outputs)
+};
+
+enum FoldKind : int {
+    FK_FULL = 0,     // chunkwise slots with occ == C
+    FK_FORCE = 1,    // chunkwise slots with occ > 0; direct slots: compress, S0 = 0
+    FK_COMMIT = 2,   // chunkwise: n = occ + clamp(n_acc[r], 0, n_draft)
+};
+
+struct FoldArgs {
+    Dims dm;
+    Ptrs p;
+    int first, n;
+    int kind;
+    const int *nacc;    // FK_COMMIT
+    int n_draft;
+};
+
+struct RecArgs {
+    Dims dm;
+    Ptrs p;
+    int first, n;
+    int n_draft;        // 1 for the decode step
+    const void *q, *k, *v;
+    const float *alpha, *beta;
+    float *o;
+    float *temp;        // recurrent verify: [n][n_draft][Hv][d][d]
+    const int *nacc;    // recurrent commit
+};
+
+// Launchers: return cudaSuccess or the launch error; *launches += kernels.
+cudaError_t launch_chunk(const ChunkArgs &a, cudaStream_t s, int64_t *launches);
+cudaError_t launch_fold(const FoldArgs &a, cudaStream_t s, int64_t *launches);
+cudaError_t launch_recurrent_step(const RecArgs &a, cudaStream_t s, int64_t *launches);
+cudaError_t launch_recurrent_verify(const RecArgs &a, cudaStream_t s, int64_t *launches);
+cudaError_t launch_recurrent_commit(const RecArgs &a, cudaStream_t s, int64_t *launches);
+cudaError_t launch_reset(const Dims &dm, const Ptrs &p, int first, int n, int mode, int zero_state,
+                         cudaStream_t s, int64_t *launches);
+
+}  // namespace labuf

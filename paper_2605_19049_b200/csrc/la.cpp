@@ -1,0 +1,488 @@
+// la.cpp — host side of the C ABI declared in include/la.h: configuration
+// validation, sizing, the opaque handle with its exact host occupancy mirror,
+// all-or-nothing argument checking, and kernel launches on the caller's
+// stream.  No device memory is allocated here and nothing synchronises
+// except la_device_status.
+#include "../../include/la.h"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+
+using namespace labuf;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+la_status fail(la_status st, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+    return st;
+}
+
+la_status cuda_fail(cudaError_t e, const char *what) {
+    return fail(LA_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+size_t round_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+size_t dt_size(int dt) { return dt == LA_DT_F32 ? 4 : 2; }
+
+constexpr size_t kAlign = 1024;
+
+}  // namespace
+
+la_status labuf_set_error(la_status st, const char *msg) { return fail(st, "%s", msg); }
+
+struct la_buf {
+    la_config cfg;
+    la_sizes sz;
+    Dims dm;
+    Ptrs p;
+    int device;
+    std::vector<int32_t> occ, len, mode, pending;   // host mirror
+    int64_t launches = 0;
+};
+
+namespace {
+
+la_status check_config(const la_config *c) {
+    if (!c) return fail(LA_ERR_INVALID, "null config");
+    if (c->max_slots < 1) return fail(LA_ERR_INVALID, "max_slots must be >= 1");
+    if (c->n_qk_heads < 1 || c->n_v_heads < 1) return fail(LA_ERR_INVALID, "head counts must be >= 1");
+    if (c->d_k != kD || c->d_v != kD) return fail(LA_ERR_UNSUPPORTED, "d_k = d_v = 128 only (got %d, %d)", c->d_k, c->d_v);
+    if (c->n_v_heads % c->n_qk_heads != 0) return fail(LA_ERR_UNSUPPORTED, "n_v_heads %% n_qk_heads != 0");
+    const int g = c->n_v_heads / c->n_qk_heads;
+    if (g != 1 && g != 2 && g != 4) return fail(LA_ERR_UNSUPPORTED, "n_v_heads / n_qk_heads must be 1, 2 or 4");
+    if (c->chunk < 1 || c->chunk > 64) return fail(LA_ERR_INVALID, "chunk must be in [1, 64]");
+    if (c->max_drafts < 0 || c->max_drafts > kMaxNewPerLaunch) return fail(LA_ERR_INVALID, "max_drafts must be in [0, 16]");
+    if (c->short_cap < 0 || c->short_cap > kD) return fail(LA_ERR_INVALID, "short_cap must be in [0, 128]");
+    if (c->in_dtype != LA_DT_F32 && c->in_dtype != LA_DT_BF16) return fail(LA_ERR_UNSUPPORTED, "in_dtype must be F32 or BF16");
+    if (c->u_dtype != LA_DT_F32 && c->u_dtype != LA_DT_F16) return fail(LA_ERR_UNSUPPORTED, "u_dtype must be F32 or F16 (never BF16, reading Z11)");
+    if (c->u_dtype == LA_DT_F16 && c->in_dtype != LA_DT_BF16) return fail(LA_ERR_UNSUPPORTED, "u_dtype F16 requires in_dtype BF16");
+    if (c->keep_raw != 0 && c->keep_raw != 1) return fail(LA_ERR_INVALID, "keep_raw must be 0 or 1");
+    if (c->validate != 0 && c->validate != 1) return fail(LA_ERR_INVALID, "validate must be 0 or 1");
+    return LA_OK;
+}
+
+void compute_sizes(const la_config *c, la_sizes *s) {
+    memset(s, 0, sizeof(*s));
+    const size_t R = c->max_slots, Hk = c->n_qk_heads, Hv = c->n_v_heads, d = kD;
+    const int T = std::max(c->chunk + c->max_drafts, c->short_cap);
+    s->capacity = T;
+    s->align = kAlign;
+    s->state_bytes = R * Hv * d * d * 4;
+    size_t o = 0;
+    s->off_k = o; o = round_up(o + R * Hk * T * d * dt_size(c->in_dtype), kAlign);
+    s->off_u = o; o = round_up(o + R * Hv * T * d * dt_size(c->u_dtype), kAlign);
+    s->off_g = o; o = round_up(o + R * Hv * T * 4, kAlign);
+    if (c->keep_raw) {
+        s->off_v = o; o = round_up(o + R * Hv * T * d * dt_size(c->in_dtype), kAlign);
+        s->off_b = o; o = round_up(o + R * Hv * T * 4, kAlign);
+    }
+    s->buffer_bytes = o;
+    s->meta_bytes = round_up(4 * R * 4 + 16, 256);
+    s->record_bytes = Hk * d * dt_size(c->in_dtype) + Hv * d * dt_size(c->u_dtype) + Hv * 4 +
+                      (c->keep_raw ? Hv * d * dt_size(c->in_dtype) + Hv * 4 : 0);
+}
+
+bool aligned(const void *p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
+
+la_status check_handle(la_buf *b) {
+    if (!b) return fail(LA_ERR_INVALID, "null handle");
+    return LA_OK;
+}
+
+la_status check_range(la_buf *b, int32_t first, int32_t n) {
+    if (first < 0 || n < 0 || (int64_t)first + n > b->cfg.max_slots)
+        return fail(LA_ERR_INVALID, "slot range [%d, %d) outside [0, %d)", first, first + n, b->cfg.max_slots);
+    return LA_OK;
+}
+
+la_status check_inputs(const void *q, const void *k, const void *v, const float *alpha,
+                       const float *beta, const float *o, bool o_required) {
+    if (!q || !k || !v || !alpha || !beta) return fail(LA_ERR_INVALID, "null input pointer");
+    if (o_required && !o) return fail(LA_ERR_INVALID, "null output pointer");
+    if (!aligned(q, 16) || !aligned(k, 16) || !aligned(v, 16) || !aligned(alpha, 4) ||
+        !aligned(beta, 4) || (o && !aligned(o, 16)))
+        return fail(LA_ERR_INVALID, "inputs must be 16-byte aligned");
+    return LA_OK;
+}
+
+la_status set_device(la_buf *b) {
+    int cur = -1;
+    cudaError_t e = cudaGetDevice(&cur);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    if (cur != b->device) {
+        e = cudaSetDevice(b->device);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+    }
+    return LA_OK;
+}
+
+ChunkArgs chunk_args(la_buf *b, int first, int n, int n_new, int j0_cap, int tok_total,
+                     int tok_offset, int kind, const void *q, const void *k, const void *v,
+                     const float *alpha, const float *beta, float *o) {
+    ChunkArgs a;
+    a.dm = b->dm; a.p = b->p;
+    a.first = first; a.n = n; a.n_new = n_new; a.j0_cap = j0_cap;
+    a.tok_total = tok_total; a.tok_offset = tok_offset; a.kind = kind;
+    a.q = q; a.k = k; a.v = v; a.alpha = alpha; a.beta = beta; a.o = o;
+    return a;
+}
+
+}  // namespace
+
+extern "C" {
+
+la_status la_buf_query(const la_config *cfg, la_sizes *out) {
+    la_status st = check_config(cfg);
+    if (st != LA_OK) return st;
+    if (!out) return fail(LA_ERR_INVALID, "null sizes output");
+    compute_sizes(cfg, out);
+    return LA_OK;
+}
+
+la_status la_buf_create(const la_config *cfg, void *state, void *buffer, void *meta, int32_t device,
+                        la_buf **out) {
+    la_status st = check_config(cfg);
+    if (st != LA_OK) return st;
+    if (!out) return fail(LA_ERR_INVALID, "null handle output");
+    if (!state || !buffer || !meta) return fail(LA_ERR_INVALID, "null device pointer");
+    if (!aligned(state, kAlign) || !aligned(buffer, kAlign) || !aligned(meta, 256))
+        return fail(LA_ERR_INVALID, "state/buffer must be 1024-byte aligned, meta 256-byte aligned");
+    if (device < 0) return fail(LA_ERR_INVALID, "bad device ordinal");
+    la_buf *b = new la_buf();
+    b->cfg = *cfg;
+    compute_sizes(cfg, &b->sz);
+    b->device = device;
+    Dims &dm = b->dm;
+    dm.R = cfg->max_slots; dm.Hk = cfg->n_qk_heads; dm.Hv = cfg->n_v_heads;
+    dm.g = cfg->n_v_heads / cfg->n_qk_heads; dm.T = b->sz.capacity; dm.C = cfg->chunk;
+    dm.in_dt = cfg->in_dtype; dm.u_dt = cfg->u_dtype; dm.keep_raw = cfg->keep_raw;
+    dm.validate = cfg->validate;
+    Ptrs &p = b->p;
+    char *bb = static_cast<char *>(buffer);
+    p.state = static_cast<float *>(state);
+    p.K = bb + b->sz.off_k;
+    p.U = bb + b->sz.off_u;
+    p.G = reinterpret_cast<float *>(bb + b->sz.off_g);
+    p.V = cfg->keep_raw ? bb + b->sz.off_v : nullptr;
+    p.B = cfg->keep_raw ? reinterpret_cast<float *>(bb + b->sz.off_b) : nullptr;
+    int32_t *m = static_cast<int32_t *>(meta);
+    const int R = cfg->max_slots;
+    p.occ = m; p.len = m + R; p.mode = m + 2 * R; p.ticket = m + 3 * R;
+    p.status = reinterpret_cast<unsigned *>(m + 4 * R);
+    b->occ.assign(R, 0); b->len.assign(R, 0); b->mode.assign(R, 0); b->pending.assign(R, 0);
+    *out = b;
+    return LA_OK;
+}
+
+la_status la_buf_destroy(la_buf *buf) {
+    if (!buf) return fail(LA_ERR_INVALID, "null handle");
+    delete buf;
+    return LA_OK;
+}
+
+la_status la_request_reset(la_buf *b, int32_t first, int32_t n, int32_t mode, int32_t zero_state,
+                           la_stream stream) {
+    la_status st;
+    if ((st = check_handle(b)) != LA_OK || (st = check_range(b, first, n)) != LA_OK) return st;
+    if (mode != LA_MODE_CHUNKWISE && mode != LA_MODE_DIRECT) return fail(LA_ERR_INVALID, "bad mode");
+    if (mode == LA_MODE_DIRECT && b->cfg.short_cap == 0) return fail(LA_ERR_MODE, "direct mode disabled (short_cap = 0)");
+    if (n == 0) return LA_OK;
+    if ((st = set_device(b)) != LA_OK) return st;
+    cudaError_t e = launch_reset(b->dm, b->p, first, n, mode, zero_state ? 1 : 0,
+                                 static_cast<cudaStream_t>(stream), &b->launches);
+    if (e != cudaSuccess) return cuda_fail(e, "reset launch");
+    // status word: cleared by a reset covering slot 0
+    if (first == 0) {
+        e = cudaMemsetAsync(b->p.status, 0, sizeof(unsigned), static_cast<cudaStream_t>(stream));
+        if (e != cudaSuccess) return cuda_fail(e, "status clear");
+    }
+    for (int r = first; r < first + n; ++r) {
+        b->occ[r] = 0; b->len[r] = 0; b->mode[r] = mode; b->pending[r] = 0;
+    }
+    return LA_OK;
+}
+
+la_status la_decode_step(la_buf *b, int32_t first, int32_t n, const void *q, const void *k,
+                         const void *v, const float *alpha, const float *beta, float *o,
+                         la_stream stream) {
+    la_status st;
+    if ((st = check_handle(b)) != LA_OK || (st = check_range(b, first, n)) != LA_OK) return st;
+    if ((st = check_inputs(q, k, v, alpha, beta, o, true)) != LA_OK) return st;
+    int j0_cap = 0;
+    for (int r = first; r < first + n; ++r) {
+        if (b->mode[r] != LA_MODE_CHUNKWISE) return fail(LA_ERR_MODE, "slot %d is not CHUNKWISE", r);
+        if (b->pending[r]) return fail(LA_ERR_MODE, "slot %d has a pending verify (commit first)", r);
+        if (b->occ[r] >= b->cfg.chunk) return fail(LA_ERR_CAPACITY, "slot %d buffer full (call la_flush)", r);
+        j0_cap = std::max(j0_cap, b->occ[r]);
+    }
+    if (n == 0) return LA_OK;
+    if ((st = set_device(b)) != LA_OK) return st;
+    ChunkArgs a = chunk_args(b, first, n, 1, j0_cap, 1, 0, CK_DECODE, q, k, v, alpha, beta, o);
+    cudaError_t e = launch_chunk(a, static_cast<cudaStream_t>(stream), &b->launches);
+    if (e != cudaSuccess) return cuda_fail(e, "decode launch");
+    for (int r = first; r < first + n; ++r) b->occ[r] += 1;
+    return LA_OK;
+}
+
+la_status la_flush(la_buf *b, int32_t first, int32_t n, int32_t kind, la_stream stream) {
+    la_status st;
+    if ((st = check_handle(b)) != LA_OK || (st = check_range(b, first, n)) != LA_OK) return st;
+    if (kind != LA_FLUSH_FULL && kind != LA_FLUSH_FORCE) return fail(LA_ERR_INVALID, "bad flush kind");
+    bool any = false;
+    for (int r = first; r < first + n; ++r) {
+        if (b->pending[r]) return fail(LA_ERR_MODE, "slot %d has a pending verify (commit first)", r);
+        if (kind == LA_FLUSH_FULL)
+            any |= (b->mode[r] == LA_MODE_CHUNKWISE && b->occ[r] == b->cfg.chunk);
+        else
+            any |= (b->mode[r] == LA_MODE_CHUNKWISE ? b->occ[r] > 0 : b->len[r] > 0);
+    }
+    if (!any) return LA_OK;   // empty flush is not an error (SPEC flush_and_free)
+    if ((st = set_device(b)) != LA_OK) return st;
+    FoldArgs a;
+    a.dm = b->dm; a.p = b->p; a.first = first; a.n = n;
+    a.kind = kind == LA_FLUSH_FULL ? FK_FULL : FK_FORCE; a.nacc = nullptr; a.n_draft = 0;
+    cudaError_t e = launch_fold(a, static_cast<cudaStream_t>(stream), &b->launches);
+    if (e != cudaSuccess) return cuda_fail(e, "flush launch");
+    for (int r = first; r < first + n; ++r) {
+        if (kind == LA_FLUSH_FULL) {
+            if (b->mode[r] == LA_MODE_CHUNKWISE && b->occ[r] == b->cfg.chunk) b->occ[r] = 0;
+        } else if (b->mode[r] == LA_MODE_CHUNKWISE) {
+            b->occ[r] = 0;
+        } else if (b->len[r] > 0) {
+            b->mode[r] = LA_MODE_CHUNKWISE; b->len[r] = 0; b->occ[r] = 0;
+        }
+    }
+    return LA_OK;
+}
+
+la_status la_verify_drafts(la_buf *b, int32_t first, int32_t n, int32_t n_draft, const void *q,
+                           const void *k, const void *v, const float *alpha, const float *beta,
+                           float *o, la_stream stream) {
+    la_status st;
+    if ((st = check_handle(b)) != LA_OK || (st = check_range(b, first, n)) != LA_OK) return st;
+    if ((st = check_inputs(q, k, v, alpha, beta, o, true)) != LA_OK) return st;
+    if (n_draft < 1 || n_draft > b->cfg.max_drafts)
+        return fail(LA_ERR_INVALID, "n_draft %d outside [1, %d]", n_draft, b->cfg.max_drafts);
+    int j0_cap = 0;
+    for (int r = first; r < first + n; ++r) {
+        if (b->mode[r] != LA_MODE_CHUNKWISE) return fail(LA_ERR_MODE, "slot %d is not CHUNKWISE", r);
+        if (b->pending[r]) return fail(LA_ERR_MODE, "slot %d already has a pending verify", r);
+        if (b->occ[r] + n_draft > b->sz.capacity) return fail(LA_ERR_CAPACITY, "slot %d: occ + n_draft > capacity", r);
+        j0_cap = std::max(j0_cap, b->occ[r]);
+    }
+    if (n == 0) return LA_OK;
+    if ((st = set_device(b)) != LA_OK) return st;
+    ChunkArgs a = chunk_args(b, first, n, n_draft, j0_cap, n_draft, 0, CK_VERIFY, q, k, v, alpha, beta, o);
+    cudaError_t e = launch_chunk(a, static_cast<cudaStream_t>(stream), &b->launches);
+    if (e != cudaSuccess) return cuda_fail(e, "verify launch");
+    for (int r = first; r < first + n; ++r) b->pending[r] = n_draft;
+    return LA_OK;
+}
+
+la_status la_commit_accepted(la_buf *b, int32_t first, int32_t n, const int32_t *n_accepted,
+                             la_stream stream) {
+    la_status st;
+    if ((st = check_handle(b)) != LA_OK || (st = check_range(b, first, n)) != LA_OK) return st;
+    if (!n_accepted) return fail(LA_ERR_INVALID, "null n_accepted");
+    if (n == 0) return LA_OK;
+    const int nd = b->pending[first];
+    for (int r = first; r < first + n; ++r)
+        if (b->pending[r] == 0 || b->pending[r] != nd)
+            return fail(LA_ERR_MODE, "slot %d has no pending verify of %d drafts", r, nd);
+    if ((st = set_device(b)) != LA_OK) return st;
+    FoldArgs a;
+    a.dm = b->dm; a.p = b->p; a.first = first; a.n = n;
+    a.kind = FK_COMMIT; a.nacc = n_accepted; a.n_draft = nd;
+    cudaError_t e = launch_fold(a, static_cast<cudaStream_t>(stream), &b->launches);
+    if (e != cudaSuccess) return cuda_fail(e, "commit launch");
+    for (int r = first; r < first + n; ++r) { b->occ[r] = 0; b->pending[r] = 0; }
+    return LA_OK;
+}
+
+la_status la_direct_short(la_buf *b, int32_t first, int32_t n, int32_t n_new, const void *q,
+                          const void *k, const void *v, const float *alpha, const float *beta,
+                          float *o, la_stream stream) {
+    la_status st;
+    if ((st = check_handle(b)) != LA_OK || (st = check_range(b, first, n)) != LA_OK) return st;
+    if ((st = check_inputs(q, k, v, alpha, beta, o, true)) != LA_OK) return st;
+    if (n_new < 1) return fail(LA_ERR_INVALID, "n_new must be >= 1");
+    int j0_cap = 0;
+    for (int r = first; r < first + n; ++r) {
+        if (b->mode[r] != LA_MODE_DIRECT) return fail(LA_ERR_MODE, "slot %d is not DIRECT", r);
+        if (b->len[r] + n_new > b->cfg.short_cap) return fail(LA_ERR_CAPACITY, "slot %d: len + n_new > short_cap", r);
+        j0_cap = std::max(j0_cap, b->len[r]);
+    }
+    if (n == 0) return LA_OK;
+    if ((st = set_device(b)) != LA_OK) return st;
+    for (int off = 0; off < n_new; off += kMaxNewPerLaunch) {
+        const int m = std::min(kMaxNewPerLaunch, n_new - off);
+        ChunkArgs a = chunk_args(b, first, n, m, j0_cap + off, n_new, off, CK_DIRECT, q, k, v, alpha, beta, o);
+        cudaError_t e = launch_chunk(a, static_cast<cudaStream_t>(stream), &b->launches);
+        if (e != cudaSuccess) return cuda_fail(e, "direct launch");
+    }
+    for (int r = first; r < first + n; ++r) b->len[r] += n_new;
+    return LA_OK;
+}
+
+la_status la_prefill(la_buf *b, int32_t first, int32_t n, int32_t n_tok, const void *q, const void *k,
+                     const void *v, const float *alpha, const float *beta, float *o, la_stream stream) {
+    la_status st;
+    if ((st = check_handle(b)) != LA_OK || (st = check_range(b, first, n)) != LA_OK) return st;
+    if ((st = check_inputs(q, k, v, alpha, beta, o, false)) != LA_OK) return st;
+    if (n_tok < 0) return fail(LA_ERR_INVALID, "n_tok must be >= 0");
+    for (int r = first; r < first + n; ++r) {
+        if (b->mode[r] != LA_MODE_CHUNKWISE) return fail(LA_ERR_MODE, "slot %d is not CHUNKWISE", r);
+        if (b->pending[r]) return fail(LA_ERR_MODE, "slot %d has a pending verify", r);
+        if (b->occ[r] != 0) return fail(LA_ERR_MODE, "slot %d: prefill needs an empty buffer (occ = %d)", r, b->occ[r]);
+    }
+    if (n == 0 || n_tok == 0) return LA_OK;
+    if ((st = set_device(b)) != LA_OK) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int C = b->cfg.chunk;
+    for (int c0 = 0; c0 < n_tok; c0 += C) {
+        const int cn = std::min(C, n_tok - c0);
+        for (int off = 0; off < cn; off += kMaxNewPerLaunch) {
+            const int m = std::min(kMaxNewPerLaunch, cn - off);
+            ChunkArgs a = chunk_args(b, first, n, m, off, n_tok, c0 + off, CK_PREFILL, q, k, v, alpha, beta, o);
+            cudaError_t e = launch_chunk(a, s, &b->launches);
+            if (e != cudaSuccess) return cuda_fail(e, "prefill chunk launch");
+        }
+        FoldArgs f;
+        f.dm = b->dm; f.p = b->p; f.first = first; f.n = n; f.kind = FK_FORCE; f.nacc = nullptr; f.n_draft = 0;
+        cudaError_t e = launch_fold(f, s, &b->launches);
+        if (e != cudaSuccess) return cuda_fail(e, "prefill fold launch");
+    }
+    return LA_OK;
+}
+
+la_status la_recurrent_step(la_buf *b, int32_t first, int32_t n, const void *q, const void *k,
+                            const void *v, const float *alpha, const float *beta, float *o,
+                            la_stream stream) {
+    la_status st;
+    if ((st = check_handle(b)) != LA_OK || (st = check_range(b, first, n)) != LA_OK) return st;
+    if ((st = check_inputs(q, k, v, alpha, beta, o, true)) != LA_OK) return st;
+    for (int r = first; r < first + n; ++r)
+        if (b->mode[r] != LA_MODE_CHUNKWISE || b->occ[r] != 0 || b->pending[r])
+            return fail(LA_ERR_MODE, "slot %d: recurrent step needs a CHUNKWISE slot with an empty buffer", r);
+    if (n == 0) return LA_OK;
+    if ((st = set_device(b)) != LA_OK) return st;
+    RecArgs a{};
+    a.dm = b->dm; a.p = b->p; a.first = first; a.n = n; a.n_draft = 1;
+    a.q = q; a.k = k; a.v = v; a.alpha = alpha; a.beta = beta; a.o = o;
+    cudaError_t e = launch_recurrent_step(a, static_cast<cudaStream_t>(stream), &b->launches);
+    if (e != cudaSuccess) return cuda_fail(e, "recurrent step launch");
+    return LA_OK;
+}
+
+la_status la_recurrent_verify(la_buf *b, int32_t first, int32_t n, int32_t n_draft, const void *q,
+                              const void *k, const void *v, const float *alpha, const float *beta,
+                              float *temp, float *o, la_stream stream) {
+    la_status st;
+    if ((st = check_handle(b)) != LA_OK || (st = check_range(b, first, n)) != LA_OK) return st;
+    if ((st = check_inputs(q, k, v, alpha, beta, o, true)) != LA_OK) return st;
+    if (!temp || !aligned(temp, 16)) return fail(LA_ERR_INVALID, "temp must be a 16-byte aligned device pointer");
+    if (n_draft < 1 || n_draft > kMaxNewPerLaunch) return fail(LA_ERR_INVALID, "n_draft outside [1, 16]");
+    for (int r = first; r < first + n; ++r)
+        if (b->mode[r] != LA_MODE_CHUNKWISE || b->occ[r] != 0 || b->pending[r])
+            return fail(LA_ERR_MODE, "slot %d: recurrent verify needs a CHUNKWISE slot with an empty buffer", r);
+    if (n == 0) return LA_OK;
+    if ((st = set_device(b)) != LA_OK) return st;
+    RecArgs a{};
+    a.dm = b->dm; a.p = b->p; a.first = first; a.n = n; a.n_draft = n_draft;
+    a.q = q; a.k = k; a.v = v; a.alpha = alpha; a.beta = beta; a.o = o; a.temp = temp;
+    cudaError_t e = launch_recurrent_verify(a, static_cast<cudaStream_t>(stream), &b->launches);
+    if (e != cudaSuccess) return cuda_fail(e, "recurrent verify launch");
+    return LA_OK;
+}
+
+la_status la_recurrent_commit(la_buf *b, int32_t first, int32_t n, int32_t n_draft,
+                              const int32_t *n_accepted, const float *temp, la_stream stream) {
+    la_status st;
+    if ((st = check_handle(b)) != LA_OK || (st = check_range(b, first, n)) != LA_OK) return st;
+    if (!n_accepted || !temp || !aligned(temp, 16)) return fail(LA_ERR_INVALID, "null/misaligned pointer");
+    if (n_draft < 1 || n_draft > kMaxNewPerLaunch) return fail(LA_ERR_INVALID, "n_draft outside [1, 16]");
+    if (n == 0) return LA_OK;
+    if ((st = set_device(b)) != LA_OK) return st;
+    RecArgs a{};
+    a.dm = b->dm; a.p = b->p; a.first = first; a.n = n; a.n_draft = n_draft;
+    a.nacc = n_accepted; a.temp = const_cast<float *>(temp);
+    cudaError_t e = launch_recurrent_commit(a, static_cast<cudaStream_t>(stream), &b->launches);
+    if (e != cudaSuccess) return cuda_fail(e, "recurrent commit launch");
+    return LA_OK;
+}
+
+la_status la_state_get(la_buf *b, int32_t slot, float *dst, la_stream stream) {
+    la_status st;
+    if ((st = check_handle(b)) != LA_OK || (st = check_range(b, slot, 1)) != LA_OK) return st;
+    if (!dst) return fail(LA_ERR_INVALID, "null dst");
+    if ((st = set_device(b)) != LA_OK) return st;
+    const size_t bytes = (size_t)b->dm.Hv * kD * kD * 4;
+    cudaError_t e = cudaMemcpyAsync(dst, b->p.state + (size_t)slot * b->dm.Hv * kD * kD, bytes,
+                                    cudaMemcpyDeviceToDevice, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "state_get copy");
+    return LA_OK;
+}
+
+la_status la_state_set(la_buf *b, int32_t slot, const float *src, la_stream stream) {
+    la_status st;
+    if ((st = check_handle(b)) != LA_OK || (st = check_range(b, slot, 1)) != LA_OK) return st;
+    if (!src) return fail(LA_ERR_INVALID, "null src");
+    if ((st = set_device(b)) != LA_OK) return st;
+    const size_t bytes = (size_t)b->dm.Hv * kD * kD * 4;
+    cudaError_t e = cudaMemcpyAsync(b->p.state + (size_t)slot * b->dm.Hv * kD * kD, src, bytes,
+                                    cudaMemcpyDeviceToDevice, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "state_set copy");
+    return LA_OK;
+}
+
+la_status la_slot_info(la_buf *b, int32_t slot, int32_t *occ, int32_t *len, int32_t *mode,
+                       int32_t *pending_drafts) {
+    la_status st;
+    if ((st = check_handle(b)) != LA_OK || (st = check_range(b, slot, 1)) != LA_OK) return st;
+    if (occ) *occ = b->occ[slot];
+    if (len) *len = b->len[slot];
+    if (mode) *mode = b->mode[slot];
+    if (pending_drafts) *pending_drafts = b->pending[slot];
+    return LA_OK;
+}
+
+la_status la_device_status(la_buf *b, la_stream stream, uint32_t *flags, int32_t *occ_host,
+                           int32_t *len_host, int32_t *mode_host) {
+    la_status st;
+    if ((st = check_handle(b)) != LA_OK) return st;
+    if ((st = set_device(b)) != LA_OK) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    cudaError_t e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_fail(e, "stream synchronize");
+    const int R = b->cfg.max_slots;
+    unsigned f = 0;
+    e = cudaMemcpy(&f, b->p.status, sizeof(unsigned), cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess && occ_host) e = cudaMemcpy(occ_host, b->p.occ, R * 4, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess && len_host) e = cudaMemcpy(len_host, b->p.len, R * 4, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess && mode_host) e = cudaMemcpy(mode_host, b->p.mode, R * 4, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_fail(e, "status read");
+    if (flags) *flags = f;
+    return LA_OK;
+}
+
+int64_t la_kernel_launches(const la_buf *b) { return b ? b->launches : -1; }
+
+const char *la_last_error(void) { return g_last_error.c_str(); }
+
+}  // extern "C"

@@ -1,0 +1,271 @@
+// recurrent.cu — kernels (5a) and (5b): the conventional recurrent GDN path
+// that existing serving systems run ("fused into a single
+// kernel"), kept as the in-run IO baseline.  They use the same streaming
+// machinery as kernel (1) (bulk-copy state tiles, transposed warp
+// reductions) so "buffered beats recurrent" is not a straw man.
+//
+// Row j of the state evolves independently (north-star form):
+//   m_j = alpha (S0[j] . k);  u_j = beta (v_j - m_j);
+//   S[j] <- alpha S0[j] + u_j k;  o_j = S[j] . q = alpha (S0[j] . q) + u_j (k . q)
+#include "device.cuh"
+#include "internal.h"
+
+namespace labuf {
+
+// ------------------------------------------------------------------ (5a)
+// CTA = (d_v tile of kRows rows, QK head, slot) over the g V heads of the
+// QK head.  Reads the state tile once, writes it once.
+template <typename InT, int G>
+__global__ void __launch_bounds__(256) recurrent_step_kernel(const RecArgs a) {
+    constexpr int ROWS = kRows, GR = G * ROWS, RPW = GR / 8;
+    constexpr int RG = RPW < 8 ? RPW : 8;
+    constexpr int NV = 2 * RG;
+    const int tile = blockIdx.x, hk = blockIdx.y, zi = blockIdx.z;
+    const int r = a.first + zi;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int Hv = a.dm.Hv, Hk = a.dm.Hk;
+
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smem);
+    float *S_s = reinterpret_cast<float *>(smem + 128);
+    float *av = S_s + GR * kD;       // S0 k
+    float *bv = av + GR;             // S0 q
+    float *us = bv + GR;             // u
+    float *kq = us + GR;             // k . q
+
+    float *tiles[G];
+#pragma unroll
+    for (int hh = 0; hh < G; ++hh)
+        tiles[hh] = a.p.state + (((size_t)r * Hv + hk * G + hh) * kD + (size_t)tile * ROWS) * kD;
+    if (tid == 0) {
+        mbar_init(bar, 1);
+        fence_mbar_init();
+        mbar_arrive_expect_tx(bar, GR * kD * 4);
+#pragma unroll
+        for (int hh = 0; hh < G; ++hh) bulk_g2s(S_s + hh * ROWS * kD, tiles[hh], ROWS * kD * 4, bar);
+    }
+    const InT *kin = static_cast<const InT *>(a.k) + ((size_t)zi * Hk + hk) * kD;
+    const InT *qin = static_cast<const InT *>(a.q) + ((size_t)zi * Hk + hk) * kD;
+    const float4 k4 = load4(kin + 4 * lane);
+    const float4 q4 = load4(qin + 4 * lane);
+    if (warp == 0) {
+        const float x = warp_sum(dot4(k4, q4));
+        if (lane == 0) *kq = x;
+    }
+    __syncthreads();
+    mbar_wait(bar, 0);
+    for (int rg0 = 0; rg0 < RPW; rg0 += RG) {
+        float vals[NV];
+#pragma unroll
+        for (int rr = 0; rr < RG; ++rr) {
+            const float4 s4 = reinterpret_cast<const float4 *>(S_s + (size_t)(warp * RPW + rg0 + rr) * kD)[lane];
+            vals[2 * rr] = dot4(s4, k4);
+            vals[2 * rr + 1] = dot4(s4, q4);
+        }
+        const float red = transposed_reduce<NV>(vals, lane);
+        if (lane < NV) (lane & 1 ? bv : av)[warp * RPW + rg0 + (lane >> 1)] = red;
+    }
+    __syncthreads();
+    if (tid < GR) {
+        const int hh = tid / ROWS, row = tid % ROWS, h = hk * G + hh;
+        const int drow = tile * ROWS + row;
+        const float al = a.alpha[(size_t)zi * Hv + h], be = a.beta[(size_t)zi * Hv + h];
+        const float vt = to_f(static_cast<const InT *>(a.v)[((size_t)zi * Hv + h) * kD + drow]);
+        const float u = be * (vt - al * av[tid]);
+        us[tid] = u;
+        a.o[((size_t)zi * Hv + h) * kD + drow] = fmaf(al, bv[tid], u * (*kq));
+    }
+    __syncthreads();
+    // S_new row = alpha S0 row + u k, in place, then one bulk store per head
+    for (int rr = 0; rr < RPW; ++rr) {
+        const int rf = warp * RPW + rr;
+        const int h = hk * G + rf / ROWS;
+        const float al = a.alpha[(size_t)zi * Hv + h];
+        float4 *p = reinterpret_cast<float4 *>(S_s + (size_t)rf * kD) + lane;
+        float4 s = *p;
+        const float u = us[rf];
+        s.x = fmaf(u, k4.x, al * s.x);
+        s.y = fmaf(u, k4.y, al * s.y);
+        s.z = fmaf(u, k4.z, al * s.z);
+        s.w = fmaf(u, k4.w, al * s.w);
+        *p = s;
+    }
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+#pragma unroll
+        for (int hh = 0; hh < G; ++hh) bulk_s2g(tiles[hh], S_s + hh * ROWS * kD, ROWS * kD * 4);
+        bulk_commit();
+        bulk_wait0();
+    }
+}
+
+// ------------------------------------------------------------------ (5b)
+// N sequential recurrent steps from one state read; writes N temporary
+// states [n][N][Hv][d][d] and N outputs.  Rows stay in
+// registers across steps; each warp owns RPW rows.
+template <typename InT, int G>
+__global__ void __launch_bounds__(256) recurrent_verify_kernel(const RecArgs a) {
+    constexpr int ROWS = kRows, GR = G * ROWS, RPW = GR / 8;
+    constexpr int NV = 2 * RPW;          // RPW <= 16 -> NV <= 32
+    const int tile = blockIdx.x, hk = blockIdx.y, zi = blockIdx.z;
+    const int r = a.first + zi;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int Hv = a.dm.Hv, Hk = a.dm.Hk, N = a.n_draft;
+
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smem);
+    float *S_s = reinterpret_cast<float *>(smem + 128);
+    float *ab = S_s + GR * kD;           // [8 warps][NV]
+
+    if (tid == 0) {
+        mbar_init(bar, 1);
+        fence_mbar_init();
+        mbar_arrive_expect_tx(bar, GR * kD * 4);
+#pragma unroll
+        for (int hh = 0; hh < G; ++hh)
+            bulk_g2s(S_s + hh * ROWS * kD,
+                     a.p.state + (((size_t)r * Hv + hk * G + hh) * kD + (size_t)tile * ROWS) * kD,
+                     ROWS * kD * 4, bar);
+    }
+    __syncthreads();
+    mbar_wait(bar, 0);
+    float4 s[RPW];
+#pragma unroll
+    for (int rr = 0; rr < RPW; ++rr)
+        s[rr] = reinterpret_cast<const float4 *>(S_s + (size_t)(warp * RPW + rr) * kD)[lane];
+    const InT *qin = static_cast<const InT *>(a.q);
+    const InT *kin = static_cast<const InT *>(a.k);
+    const InT *vin = static_cast<const InT *>(a.v);
+    float *mine = ab + warp * 32;
+    for (int t = 0; t < N; ++t) {
+        const size_t tok = (size_t)zi * N + t;
+        const float4 k4 = load4(kin + (tok * Hk + hk) * kD + 4 * lane);
+        const float4 q4 = load4(qin + (tok * Hk + hk) * kD + 4 * lane);
+        const float kq = warp_sum(dot4(k4, q4));
+        float vals[NV];
+#pragma unroll
+        for (int rr = 0; rr < RPW; ++rr) {
+            vals[2 * rr] = dot4(s[rr], k4);
+            vals[2 * rr + 1] = dot4(s[rr], q4);
+        }
+        const float red = transposed_reduce<NV>(vals, lane);
+        if (lane < NV) mine[lane] = red;
+        __syncwarp();
+#pragma unroll
+        for (int rr = 0; rr < RPW; ++rr) {
+            const int rf = warp * RPW + rr;
+            const int hh = rf / ROWS, row = rf % ROWS, h = hk * G + hh;
+            const int drow = tile * ROWS + row;
+            const float al = a.alpha[tok * Hv + h], be = a.beta[tok * Hv + h];
+            const float vt = to_f(vin[(tok * Hv + h) * kD + drow]);
+            const float u = be * (vt - al * mine[2 * rr]);
+            if (lane == 0) a.o[(tok * Hv + h) * kD + drow] = fmaf(al, mine[2 * rr + 1], u * kq);
+            float4 x = s[rr];
+            x.x = fmaf(u, k4.x, al * x.x);
+            x.y = fmaf(u, k4.y, al * x.y);
+            x.z = fmaf(u, k4.z, al * x.z);
+            x.w = fmaf(u, k4.w, al * x.w);
+            s[rr] = x;
+            float *dst = a.temp + ((((size_t)zi * N + t) * Hv + h) * kD + drow) * kD;
+            reinterpret_cast<float4 *>(dst)[lane] = x;
+        }
+        __syncwarp();
+    }
+}
+
+// Commit of the baseline: state <- temp[n_acc - 1] (Fig. 3).
+__global__ void __launch_bounds__(256) recurrent_commit_kernel(const RecArgs a) {
+    const int h = blockIdx.y, zi = blockIdx.z, r = a.first + zi;
+    int na = a.nacc[zi];
+    if (na < 0 || na > a.n_draft) {
+        if (a.dm.validate && threadIdx.x == 0 && blockIdx.x == 0) atomicOr(a.p.status, 0x8u);
+        na = na < 0 ? 0 : a.n_draft;
+    }
+    if (na == 0) return;
+    const float4 *src = reinterpret_cast<const float4 *>(
+        a.temp + (((size_t)zi * a.n_draft + na - 1) * a.dm.Hv + h) * kD * kD);
+    float4 *dst = reinterpret_cast<float4 *>(a.p.state + ((size_t)r * a.dm.Hv + h) * kD * kD);
+    const int per = kD * kD / 4 / gridDim.x;
+    const int base = blockIdx.x * per;
+    for (int i = threadIdx.x; i < per; i += 256) dst[base + i] = src[base + i];
+}
+
+template <int G, typename InT>
+static cudaError_t launch_rs(const RecArgs &a, cudaStream_t s) {
+    const size_t smem = 128 + (size_t)G * kRows * kD * 4 + 3 * G * kRows * 4 + 16;
+    auto kfn = recurrent_step_kernel<InT, G>;
+    cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    kfn<<<dim3(kD / kRows, a.dm.Hk, a.n), 256, smem, s>>>(a);
+    return cudaGetLastError();
+}
+template <int G, typename InT>
+static cudaError_t launch_rv(const RecArgs &a, cudaStream_t s) {
+    const size_t smem = 128 + (size_t)G * kRows * kD * 4 + 8 * 32 * 4;
+    auto kfn = recurrent_verify_kernel<InT, G>;
+    cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    kfn<<<dim3(kD / kRows, a.dm.Hk, a.n), 256, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
+template <typename InT>
+static cudaError_t dispatch_step(const RecArgs &a, cudaStream_t s, bool verify) {
+    switch (a.dm.g) {
+        case 1: return verify ? launch_rv<1, InT>(a, s) : launch_rs<1, InT>(a, s);
+        case 2: return verify ? launch_rv<2, InT>(a, s) : launch_rs<2, InT>(a, s);
+        case 4: return verify ? launch_rv<4, InT>(a, s) : launch_rs<4, InT>(a, s);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+cudaError_t launch_recurrent_step(const RecArgs &a, cudaStream_t s, int64_t *launches) {
+    if (a.n <= 0) return cudaSuccess;
+    cudaError_t e = a.dm.in_dt == DT_F32 ? dispatch_step<float>(a, s, false)
+                                         : dispatch_step<__nv_bfloat16>(a, s, false);
+    if (e == cudaSuccess) ++*launches;
+    return e;
+}
+cudaError_t launch_recurrent_verify(const RecArgs &a, cudaStream_t s, int64_t *launches) {
+    if (a.n <= 0) return cudaSuccess;
+    cudaError_t e = a.dm.in_dt == DT_F32 ? dispatch_step<float>(a, s, true)
+                                         : dispatch_step<__nv_bfloat16>(a, s, true);
+    if (e == cudaSuccess) ++*launches;
+    return e;
+}
+cudaError_t launch_recurrent_commit(const RecArgs &a, cudaStream_t s, int64_t *launches) {
+    if (a.n <= 0) return cudaSuccess;
+    recurrent_commit_kernel<<<dim3(8, a.dm.Hv, a.n), 256, 0, s>>>(a);
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) ++*launches;
+    return e;
+}
+
+// ------------------------------------------------------------------ reset
+__global__ void reset_kernel(Ptrs p, Dims dm, int first, int n, int mode, int zero_state) {
+    const int zi = blockIdx.y, r = first + zi;
+    if (zero_state) {
+        float4 *st = reinterpret_cast<float4 *>(p.state + (size_t)r * dm.Hv * kD * kD);
+        const size_t total = (size_t)dm.Hv * kD * kD / 4;
+        for (size_t i = blockIdx.x * 256 + threadIdx.x; i < total; i += (size_t)gridDim.x * 256)
+            st[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        p.occ[r] = 0;
+        p.len[r] = 0;
+        p.mode[r] = mode;
+        p.ticket[r] = 0;
+    }
+}
+
+cudaError_t launch_reset(const Dims &dm, const Ptrs &p, int first, int n, int mode, int zero_state,
+                         cudaStream_t s, int64_t *launches) {
+    if (n <= 0) return cudaSuccess;
+    reset_kernel<<<dim3(zero_state ? 32 : 1, n), 256, 0, s>>>(p, dm, first, n, mode, zero_state);
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) ++*launches;
+    return e;
+}
+
+}  // namespace labuf
