@@ -1,0 +1,596 @@
+#!/usr/bin/env python
+"""bench.py — KV-buffered Gated DeltaNet decode on B200 (arxiv 2605.19049).
+
+Headline workload (BASELINE.json configs[1], "config 2"): one Qwen3-Next GDN
+layer (16 QK heads, 32 V heads, d = 128, fp32 state, bf16 q/k/v, fp32 delta
+values) decoding a batch of 64 requests with synthetic 32K-context states,
+buffer C = 16.  A *step* is one full buffer cycle of the whole hot path for
+that batch: C buffered decode steps (kernel 1) followed by the tensor-core
+flush (kernel 2), run over NL = 8 independent layer instances so the state
+working set (8 x 128 MiB) is 8x the 126 MB L2 and every state read comes
+from HBM (as in a 36-layer model).  The recurrent baseline (kernel 5a) runs
+the same tokens through the same layers in the same process.
+
+Metric (BASELINE.json): GDN decode us/token & tokens/s; value = tokens/s of
+one GDN layer summed over all GPUs = n_gpus * B / (us per decode step per
+layer), where us per step is the cycle average including the flush (Fig. 4
+caption).  Extra measured rows: parallel verify + accepted-prefix
+commit (config 3 shape) and direct short-context decode (config 4 shape).
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "GDN decode us/token & tokens/s per GPU; % of 8 TB/s HBM vs recurrent baseline"
+UNIT = "tokens/s (one GDN layer, all GPUs)"
+D = 128
+
+
+def parse_args():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=60)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="labuf", choices=["labuf", "reference"])
+    p.add_argument("--batch", type=int, default=64, help="requests per GPU")
+    p.add_argument("--chunk", type=int, default=16)
+    p.add_argument("--layers", type=int, default=8, help="layer instances rotated per step")
+    p.add_argument("--in-dtype", default="bf16", choices=["bf16", "f32"])
+    p.add_argument("--u-dtype", default="f32", choices=["f32", "f16"])
+    p.add_argument("--no-rows", action="store_true", help="skip the verify / direct rows")
+    p.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    p.add_argument("--seed", type=int, default=1002)
+    return p.parse_args()
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi sampling of SM clocks and throttle reasons during the run."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,utilization.gpu,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append((time.time(), parts))
+
+    def mark(self):
+        return time.time()
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self, t0=None, t1=None):
+        rows = [r for t, r in self.rows if (t0 is None or t >= t0) and (t1 is None or t <= t1)]
+        if not rows:
+            rows = [r for _, r in self.rows]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+        loaded = [r for r in rows if (num(r[2]) or 0) > 0] or rows
+        sm = [num(r[0]) for r in loaded if num(r[0]) is not None]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in rows for n, v in zip(names, r[4:8]) if v.strip() == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": num(rows[0][1]), "reasons": reasons, "samples": len(loaded)}
+
+
+# ---------------------------------------------------------------- helpers
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            j = json.load(f)
+        return float(j["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(kernel_key):
+    """DRAM bytes per launch from the committed ncu --set full summary, if any."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(path):
+        return None
+    try:
+        with open(path) as f:
+            return json.load(f).get(kernel_key)
+    except Exception:
+        return None
+
+
+def make_inputs(torch, B, Hk, Hv, n, in_dtype, gen, device):
+    """Seeded synthetic decode inputs with the recipe of synth/ (DESIGN.md
+    'Input recipe'), drawn on the device by torch's generator for speed."""
+    tdt = torch.bfloat16 if in_dtype == "bf16" else torch.float32
+    out = []
+    for _ in range(n):
+        q = torch.randn(B, Hk, D, generator=gen, device=device)
+        q = q / q.norm(dim=-1, keepdim=True) / D ** 0.5
+        k = torch.randn(B, Hk, D, generator=gen, device=device)
+        k = k / k.norm(dim=-1, keepdim=True)
+        v = torch.randn(B, Hv, D, generator=gen, device=device)
+        a = 1.0 - 0.1 * torch.rand(B, Hv, generator=gen, device=device)
+        b = torch.sigmoid(torch.randn(B, Hv, generator=gen, device=device))
+        out.append({"q": q.to(tdt).contiguous(), "k": k.to(tdt).contiguous(),
+                    "v": v.to(tdt).contiguous(), "alpha": a.contiguous(), "beta": b.contiguous(),
+                    "o": torch.empty(B, Hv, D, dtype=torch.float32, device=device)})
+    return out
+
+
+def fill_states(torch, bufs, gen):
+    for b in bufs:
+        st = b.state
+        st.copy_(torch.randn(st.shape, generator=gen, device=st.device) * (1.0 / (4 * D)) ** 0.5)
+
+
+def timed_graphs(torch, stream, graphs, K, W):
+    """Replay the phase graphs W times, then K times bracketed by events
+    between phases.  Returns (total_ms, [sum_ms per phase])."""
+    with torch.cuda.stream(stream):
+        for _ in range(W):
+            for g in graphs:
+                g.replay()
+    torch.cuda.synchronize()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(len(graphs) + 1)] for _ in range(K)]
+    with torch.cuda.stream(stream):
+        for k in range(K):
+            evs[k][0].record(stream)
+            for i, g in enumerate(graphs):
+                g.replay()
+                evs[k][i + 1].record(stream)
+    torch.cuda.synchronize()
+    total = evs[0][0].elapsed_time(evs[K - 1][-1])
+    phases = [sum(evs[k][i].elapsed_time(evs[k][i + 1]) for k in range(K)) for i in range(len(graphs))]
+    return total, phases
+
+
+def capture(torch, stream, fn):
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=stream):
+        fn()
+    return g
+
+
+# ---------------------------------------------------------------- CPU oracle leg
+def cpu_oracle_sample(target_s=12.0, B=64, Hk=16, Hv=32, seed=1002, max_tok=None):
+    """Time the fp64 oracle (the recurrence, as it stands) on host cores on a
+    bounded sample of the config-2 workload: B slots x Hv heads x T tokens from
+    synthetic 32K-context states.  Returns (tokens/s, cores, sample text)."""
+    import numpy as np
+    import oracle
+    import synth
+    rc = synth.Recipe(seed=seed)
+    slots = np.arange(B)
+    S0 = synth.state0(rc, slots, Hv, D, D).astype(np.float64).reshape(B * Hv, D, D)
+    cores = oracle.default_threads()
+
+    def run(T):
+        tok = synth.tokens(rc, slots, np.arange(T), Hk, Hv, D)
+        qv = synth.expand_qk_to_v_heads(tok["q"], Hv)
+        kv = synth.expand_qk_to_v_heads(tok["k"], Hv)
+        seq = lambda x: np.ascontiguousarray(np.swapaxes(x, 1, 2).reshape((B * Hv, T) + x.shape[3:]))
+        args = [seq(qv), seq(kv), seq(tok["v"]), seq(tok["alpha"]), seq(tok["beta"])]
+        t0 = time.perf_counter()
+        oracle.gdn_run(S0, *args, n_threads=cores)
+        return time.perf_counter() - t0
+
+    t1 = run(1)
+    T = max(1, int(target_s / max(t1, 1e-3)))
+    if max_tok:
+        T = min(T, max_tok)
+    dt = run(T) if T > 1 else t1
+    return B * T / dt, cores, f"{B} slots x {Hv} V heads x {T} tokens (config 2 shape, fp64 recurrence, {dt:.1f} s)"
+
+
+# ---------------------------------------------------------------- reference arm
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    # per step: one decode token of a bounded set of slots, sized so K+W steps
+    # finish in about a minute of CPU
+    import numpy as np
+    import oracle
+    import synth
+    B, Hk, Hv = args.batch, 16, 32
+    rc = synth.Recipe(seed=args.seed)
+    cores = oracle.default_threads()
+    S = synth.state0(rc, np.arange(B), Hv, D, D).astype(np.float64).reshape(B * Hv, D, D)
+
+    def step(nslots, pos):
+        slots = np.arange(nslots)
+        tok = synth.tokens(rc, slots, [pos], Hk, Hv, D)
+        qv = synth.expand_qk_to_v_heads(tok["q"], Hv)
+        kv = synth.expand_qk_to_v_heads(tok["k"], Hv)
+        seq = lambda x: np.ascontiguousarray(np.swapaxes(x, 1, 2).reshape((nslots * Hv, 1) + x.shape[3:]))
+        t0 = time.perf_counter()
+        oracle.gdn_run(S[:nslots * Hv], seq(qv), seq(kv), seq(tok["v"]), seq(tok["alpha"]),
+                       seq(tok["beta"]), n_threads=cores)
+        return time.perf_counter() - t0
+
+    t_full = step(B, 0)
+    budget = 60.0 / max(1, args.steps + args.warmup)
+    nslots = max(1, min(B, int(B * budget / max(t_full, 1e-4))))
+    for w in range(args.warmup):
+        step(nslots, 1 + w)
+    tot = 0.0
+    for k in range(args.steps):
+        tot += step(nslots, 100 + k)
+    value = nslots * args.steps / tot
+    sample = f"per step: 1 decode token x {nslots} of {B} slots x {Hv} V heads (fp64 recurrence oracle)"
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "config2: Qwen3-Next GDN layer decode, batch 64 @32K ctx (CPU oracle sample)",
+                       "batch_per_gpu": B, "chunk": args.chunk},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- main arm
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+    from paper_2605_19049_b200 import cost
+    from paper_2605_19049_b200 import labuf as L
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local if world > 1 else torch.cuda.current_device())
+    torch.cuda.set_device(dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    B, C, NL, Hk, Hv = args.batch, args.chunk, args.layers, 16, 32
+    K, W = args.steps, max(3, args.warmup)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(args.seed * 1000 + rank)
+    clocks = ClockSampler(dev.index if world == 1 else local)
+    clocks.start()
+    peak, peak_src = measured_peaks()
+    in_bytes = 2 if args.in_dtype == "bf16" else 4
+    u_bytes = 2 if args.u_dtype == "f16" else 4
+    lb = cost.LayerBytes.make(Hk, Hv, D, in_bytes, u_bytes)
+
+    cfg = L.make_config(B, Hk, Hv, chunk=C, in_dtype=args.in_dtype, u_dtype=args.u_dtype)
+    bufs = [L.LaBuf(cfg, device=dev) for _ in range(NL)]
+    for b in bufs:
+        b.reset(zero_state=False)
+    fill_states(torch, bufs, gen)
+    inputs = [make_inputs(torch, B, Hk, Hv, NL, args.in_dtype, gen, dev) for _ in range(C)]
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.synchronize()
+
+    # ---- buffered: capture decode phase (C steps x NL layers) and flush phase
+    def dec_phase():
+        for t in range(C):
+            for l, b in enumerate(bufs):
+                x = inputs[t][l]
+                b.decode_step(0, x["q"], x["k"], x["v"], x["alpha"], x["beta"], x["o"])
+
+    def flush_phase():
+        for b in bufs:
+            b.flush(0, B, L.LA_FLUSH_FULL)
+
+    n0 = sum(b.kernel_launches() for b in bufs)
+    g_dec = capture(torch, stream, dec_phase)
+    n1 = sum(b.kernel_launches() for b in bufs)
+    g_fl = capture(torch, stream, flush_phase)
+    n2 = sum(b.kernel_launches() for b in bufs)
+    launches_per_step = n2 - n0
+    dec_launches, fl_launches = n1 - n0, n2 - n1
+
+    barrier()
+    t_c0 = time.time()
+    total_ms, (dec_ms, fl_ms) = timed_graphs(torch, stream, [g_dec, g_fl], K, W)
+    barrier()
+    t_c1 = time.time()
+    total_ms = max_over_ranks(total_ms)
+    ms_per_step = total_ms / K
+    us_per_token = 1e3 * ms_per_step / (C * NL)          # one decode step of one layer, cycle avg
+    value = world * B / (us_per_token * 1e-6)
+
+    # ---- recurrent baseline (kernel 5a), same tokens, same layers
+    def rec_phase():
+        for t in range(C):
+            for l, b in enumerate(bufs):
+                x = inputs[t][l]
+                b.recurrent_step(0, x["q"], x["k"], x["v"], x["alpha"], x["beta"], x["o"])
+
+    g_rec = capture(torch, stream, rec_phase)
+    barrier()
+    rec_total, (rec_ms,) = timed_graphs(torch, stream, [g_rec], K, W)
+    barrier()
+    t_c2 = time.time()
+    rec_total = max_over_ranks(rec_total)
+    rec_us_per_token = 1e3 * rec_total / K / (C * NL)
+
+    # ---- roofline of the dominant kernel (buffered decode, kernel 1)
+    dec_bytes_per_launch = B * sum(lb.decode(j) for j in range(C)) / C
+    dec_us = 1e3 * dec_ms / (K * dec_launches)
+    fl_bytes_per_launch = B * lb.flush(C)
+    fl_us = 1e3 * fl_ms / (K * fl_launches)
+    rec_bytes_per_launch = B * lb.recurrent()
+    rec_us = 1e3 * rec_ms / (K * C * NL)
+    gbs = lambda nbytes, us: nbytes / (us * 1e-6) / 1e9
+    dec_gbs = gbs(dec_bytes_per_launch, dec_us)
+    step_bytes = NL * (B * sum(lb.decode(j) for j in range(C)) + fl_bytes_per_launch)
+    traffic = ncu_traffic("decode")
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
+        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": "config2: Qwen3-Next GDN layer decode, batch 64/GPU @32K ctx (synthetic state), C=16",
+                   "batch_per_gpu": B, "global_batch": B * world, "chunk": C, "layers_rotated": NL,
+                   "heads": {"qk": Hk, "v": Hv, "d": D}, "in_dtype": args.in_dtype, "u_dtype": args.u_dtype,
+                   "state": "fp32", "parallelism": f"dp{world} (requests partitioned, no collective)",
+                   "step": f"one buffer cycle: {C} decode steps + 1 flush, x {NL} layer instances",
+                   "l2": f"inputs larger than L2: {NL} layers x {B * lb.st / 2**20:.0f} MiB state rotated per step",
+                   "cuda_graphs": True},
+        "us_per_token": us_per_token,
+        "tokens_per_s_per_gpu": B / (us_per_token * 1e-6),
+        "hbm_frac_of_8TBs": step_bytes / (ms_per_step * 1e-3) / 8e12,
+        "hbm_frac_of_measured": step_bytes / (ms_per_step * 1e-3) / (peak * 1e9),
+        "recurrent": {"us_per_token": rec_us_per_token,
+                      "tokens_per_s_per_gpu": B / (rec_us_per_token * 1e-6),
+                      "hbm_frac_of_measured": gbs(rec_bytes_per_launch, rec_us) / peak},
+        "speedup_vs_recurrent": rec_us_per_token / us_per_token,
+        "latency_reduction_pct_vs_recurrent": 100.0 * (1 - us_per_token / rec_us_per_token),
+        "paper_context": {"latency_reduction_pct": 45.17, "capacity_x": 5,
+                          "hardware": "4x NVIDIA L40S, TP=4, SGLang v0.5.10 + Triton, FP32 state / FP16 KV (P:12, P:232, P:258, P:266)"},
+        "kernels": {
+            "decode": {"us_per_launch": dec_us, "bytes_per_launch": dec_bytes_per_launch,
+                       "gbs": dec_gbs, "launches_per_step": dec_launches},
+            "flush": {"us_per_launch": fl_us, "bytes_per_launch": fl_bytes_per_launch,
+                      "gbs": gbs(fl_bytes_per_launch, fl_us), "launches_per_step": fl_launches},
+            "recurrent_step": {"us_per_launch": rec_us, "bytes_per_launch": rec_bytes_per_launch,
+                               "gbs": gbs(rec_bytes_per_launch, rec_us)},
+        },
+        "roofline": {"bound": "hbm", "kernel": "chunk_attend_kernel (buffered decode, kernel 1)",
+                     "achieved": dec_gbs, "peak": peak, "peak_source": peak_src, "unit": "GB/s",
+                     "frac": dec_gbs / peak,
+                     "traffic": traffic,
+                     "algorithmic_bytes_per_launch": dec_bytes_per_launch,
+                     "note": "bytes = B x mean_j(st + inp + j*rec + o + rec) over occupancies j = 0..C-1"},
+        "gpu_launches": launches_per_step * K,
+    }
+
+    # ---- e2e through the public API with host buffers (pinned), eager launches
+    K_e2e = min(K, 10)
+    host_in = [[{k: v.cpu().pin_memory() for k, v in inputs[t][l].items() if k != "o"} for l in range(NL)]
+               for t in range(C)]
+    host_out = [[torch.empty(B, Hv, D, dtype=torch.float32).pin_memory() for _ in range(NL)] for _ in range(C)]
+    h2d = sum(v.numel() * v.element_size() for t in range(C) for l in range(NL) for v in host_in[t][l].values())
+    d2h = sum(x.numel() * x.element_size() for row in host_out for x in row)
+
+    def e2e_step():
+        with torch.cuda.stream(stream):
+            for t in range(C):
+                for l, b in enumerate(bufs):
+                    dst = inputs[t][l]
+                    for k_, v_ in host_in[t][l].items():
+                        dst[k_].copy_(v_, non_blocking=True)
+                    b.decode_step(0, dst["q"], dst["k"], dst["v"], dst["alpha"], dst["beta"], dst["o"])
+                    host_out[t][l].copy_(dst["o"], non_blocking=True)
+            for b in bufs:
+                b.flush(0, B, L.LA_FLUSH_FULL)
+
+    for _ in range(2):
+        e2e_step()
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(K_e2e):
+        e2e_step()
+    barrier()
+    e2e_s = max_over_ranks(time.perf_counter() - t0)
+    e2e_us_tok = 1e6 * e2e_s / K_e2e / (C * NL)
+    line["e2e"] = {"value": world * B / (e2e_us_tok * 1e-6), "unit": UNIT,
+                   "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                   "steps": K_e2e, "note": "eager la_* calls, pinned H2D of each step's q/k/v/alpha/beta and D2H of every output, wall clock"}
+
+    # ---- extra rows: verify + commit (config 3) and direct (config 4)
+    if not args.no_rows:
+        del g_dec, g_fl, g_rec
+        line["rows"] = extra_rows(torch, L, cost, dev, stream, gen, K, W, peak, args)
+
+    t_c3 = time.time()
+    clocks.stop()
+    line["clocks"] = clocks.summary(t_c0, t_c2)
+
+    if rank == 0 and world == 1 and not args.no_cpu:
+        v, cores, sample = cpu_oracle_sample(seed=args.seed)
+        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def extra_rows(torch, L, cost, dev, stream, gen, K, W, peak, args):
+    rows = {}
+    Hk, Hv = 16, 32
+    Kr = max(3, min(K, 20))
+    gbs = lambda nbytes, us: nbytes / (us * 1e-6) / 1e9
+    # ---------------- config 3: batch 256, 4 drafts, verify + commit vs recurrent verify + copy
+    import numpy as np
+    import synth
+    B3, N3, NL3 = 256, 4, 2
+    lb = cost.LayerBytes.make(Hk, Hv, D, 2, 4)
+    cfg = L.make_config(B3, Hk, Hv, chunk=16, max_drafts=N3)
+    bufs = [L.LaBuf(cfg, device=dev) for _ in range(NL3)]
+    for b in bufs:
+        b.reset(zero_state=False)
+    fill_states(torch, bufs, gen)
+    rc = synth.Recipe(seed=1003)
+    nacc = [torch.from_numpy(synth.n_accepted(rc, np.arange(B3), N3, round_idx=l)).to(dev) for l in range(NL3)]
+    tdt = torch.bfloat16
+    def drafts():
+        q = torch.randn(B3, N3, Hk, D, generator=gen, device=dev)
+        k = torch.randn(B3, N3, Hk, D, generator=gen, device=dev)
+        return {"q": (q / q.norm(dim=-1, keepdim=True) / D ** 0.5).to(tdt),
+                "k": (k / k.norm(dim=-1, keepdim=True)).to(tdt),
+                "v": torch.randn(B3, N3, Hv, D, generator=gen, device=dev).to(tdt),
+                "alpha": 1.0 - 0.1 * torch.rand(B3, N3, Hv, generator=gen, device=dev),
+                "beta": torch.sigmoid(torch.randn(B3, N3, Hv, generator=gen, device=dev)),
+                "o": torch.empty(B3, N3, Hv, D, dtype=torch.float32, device=dev)}
+    xs = [drafts() for _ in range(NL3)]
+    def ver():
+        for b, x in zip(bufs, xs):
+            b.verify_drafts(0, x["q"], x["k"], x["v"], x["alpha"], x["beta"], x["o"])
+    def com():
+        for b, na in zip(bufs, nacc):
+            b.commit_accepted(0, na)
+    gv, gc = capture(torch, stream, ver), capture(torch, stream, com)
+    tot, (v_ms, c_ms) = timed_graphs(torch, stream, [gv, gc], Kr, W)
+    us_round = 1e3 * tot / Kr / NL3
+    acc_mean = float(sum(int(n.sum()) for n in nacc)) / (NL3 * B3)
+    ver_bytes = B3 * lb.verify(N3)
+    com_bytes = sum(lb.commit(0, int(a)) for na in nacc for a in na.cpu().tolist()) / NL3
+    temps = [torch.empty(B3, N3, Hv, D, D, dtype=torch.float32, device=dev) for _ in range(NL3)]
+    def rver():
+        for b, x, tp in zip(bufs, xs, temps):
+            b.recurrent_verify(0, x["q"], x["k"], x["v"], x["alpha"], x["beta"], tp, x["o"])
+    def rcom():
+        for b, na, tp in zip(bufs, nacc, temps):
+            b.recurrent_commit(0, na, tp)
+    grv, grc = capture(torch, stream, rver), capture(torch, stream, rcom)
+    rtot, (rv_ms, rc_ms) = timed_graphs(torch, stream, [grv, grc], Kr, W)
+    rus_round = 1e3 * rtot / Kr / NL3
+    v_us = 1e3 * v_ms / Kr / NL3
+    rows["verify_commit"] = {
+        "workload": f"config3: batch {B3}, {N3} drafts, p_accept 0.7 (mean n_acc {acc_mean:.2f}), {NL3} layers rotated",
+        "us_per_round": us_round, "verify_us": v_us, "commit_us": 1e3 * c_ms / Kr / NL3,
+        "verify_gbs": gbs(ver_bytes, v_us), "verify_frac_of_measured": gbs(ver_bytes, v_us) / peak,
+        "commit_gbs": gbs(com_bytes, 1e3 * c_ms / Kr / NL3),
+        "recurrent_us_per_round": rus_round,
+        "recurrent_verify_gbs": gbs(B3 * lb.recurrent_verify(N3), 1e3 * rv_ms / Kr / NL3),
+        "speedup_vs_recurrent": rus_round / us_round,
+        "temp_state_bytes_recurrent": B3 * N3 * lb.st,
+        "capacity_requests_36_layers_180GB": {
+            "recurrent": int(180e9 // (36 * (N3 + 1) * lb.st)),
+            "buffered": int(180e9 // (36 * (lb.st + (16 + N3) * lb.rec))),
+        },
+    }
+    del gv, gc, grv, grc, temps, bufs, xs
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+
+    # ---------------- config 4: batch 1024, direct KV-only decode at context 64 -> 96
+    B4, L0, NS = 1024, 64, 32
+    cfg = L.make_config(B4, Hk, Hv, chunk=16, short_cap=128, u_dtype="f16")
+    b4 = L.LaBuf(cfg, device=dev)
+    lb4 = cost.LayerBytes.make(Hk, Hv, D, 2, 2)
+    def tok(n):
+        q = torch.randn(B4, n, Hk, D, generator=gen, device=dev)
+        k = torch.randn(B4, n, Hk, D, generator=gen, device=dev)
+        return {"q": (q / q.norm(dim=-1, keepdim=True) / D ** 0.5).to(tdt),
+                "k": (k / k.norm(dim=-1, keepdim=True)).to(tdt),
+                "v": torch.randn(B4, n, Hv, D, generator=gen, device=dev).to(tdt),
+                "alpha": 1.0 - 0.1 * torch.rand(B4, n, Hv, generator=gen, device=dev),
+                "beta": torch.sigmoid(torch.randn(B4, n, Hv, generator=gen, device=dev)),
+                "o": torch.empty(B4, n, Hv, D, dtype=torch.float32, device=dev)}
+    pre = tok(L0)
+    steps = [tok(1) for _ in range(NS)]
+    def run_direct(timed):
+        b4.reset(mode=L.LA_MODE_DIRECT, zero_state=False)
+        b4.direct_short(0, pre["q"], pre["k"], pre["v"], pre["alpha"], pre["beta"], pre["o"])
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+            for x in steps:
+                b4.direct_short(0, x["q"], x["k"], x["v"], x["alpha"], x["beta"], x["o"])
+            e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1)
+    run_direct(False)
+    d_ms = run_direct(True)
+    d_us = 1e3 * d_ms / NS
+    d_bytes = B4 * sum(lb4.direct(L0 + s) for s in range(NS)) / NS
+    # recurrent baseline at the same batch and the same tokens
+    cfgr = L.make_config(B4, Hk, Hv, chunk=16)
+    br = L.LaBuf(cfgr, device=dev)
+    br.reset(zero_state=True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for rep in range(2):
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+            for x in steps:
+                br.recurrent_step(0, x["q"][:, 0], x["k"][:, 0], x["v"][:, 0], x["alpha"][:, 0],
+                                  x["beta"][:, 0], x["o"][:, 0].contiguous())
+            e1.record(stream)
+        torch.cuda.synchronize()
+    r_us = 1e3 * e0.elapsed_time(e1) / NS
+    rows["direct"] = {
+        "workload": f"config4: batch {B4}, direct KV-only decode from context {L0} to {L0 + NS}, u fp16, no state",
+        "us_per_step": d_us, "gbs": gbs(d_bytes, d_us), "frac_of_measured": gbs(d_bytes, d_us) / peak,
+        "recurrent_us_per_step": r_us, "speedup_vs_recurrent": r_us / d_us,
+        "paper_model_speedup_vs_chunkwise_m16_at_L80": float(cost.paper_speedup_kv_only_gdn(D, 16, L0 + NS // 2)),
+    }
+    del b4, br
+    torch.cuda.empty_cache()
+    return rows
+
+
+if __name__ == "__main__":
+    main()

@@ -100,7 +100,8 @@ __global__ void __launch_bounds__(kFoldThreads) fold_kernel(const FoldArgs a) {
     }
 
     const InT *Kb = static_cast<const InT *>(a.p.K) + ((size_t)r * dm.Hk + hk) * T * kD;
-    const UT *Ub = static_cast<const UT *>(a.p.U) + ((size_t)r * Hv + h) * T * kD + (size_t)jh * kFoldNJ;
+    // U is tile-major [R][Hv][d/kUSub][T][kUSub]
+    const UT *Ub = static_cast<const UT *>(a.p.U) + ((size_t)r * Hv + h) * T * kD;
     const float *Gb = a.p.G + ((size_t)r * Hv + h) * T;
     const float g_last = Gb[n - 1];
     const uint32_t idesc = idesc_tf32(128, kFoldNJ);
@@ -129,7 +130,8 @@ __global__ void __launch_bounds__(kFoldThreads) fold_kernel(const FoldArgs a) {
             float y = 0.f;
             if (i < kn) {
                 const float w = expf(g_last - Gb[kc0 + i]);
-                y = w * to_f(Ub[(size_t)(kc0 + i) * kD + j]);
+                const int jr = jh * kFoldNJ + j;
+                y = w * to_f(Ub[((size_t)(jr / kUSub) * T + kc0 + i) * kUSub + jr % kUSub]);
             }
             const float hi = tf32_rna(y);
             const uint32_t off = kmaj_off(j, i);

@@ -7,8 +7,12 @@
 namespace labuf {
 
 constexpr int kD = 128;          // d_k = d_v
-constexpr int kRows = 32;        // d_v rows per V head per chunk-kernel CTA
+constexpr int kRows = 32;        // d_v rows per V head per recurrent-kernel CTA
+constexpr int kUSub = 32;        // U records are stored tile-major: [R][Hv][d/kUSub][T][kUSub]
 constexpr int kMaxNewPerLaunch = 16;
+constexpr int kMaxSlotsPerLaunch = 4096;
+// new tokens per chunk-kernel launch: the log-decay scan runs in one warp
+inline int max_new_per_launch(int g) { return (32 / g) < kMaxNewPerLaunch ? 32 / g : kMaxNewPerLaunch; }
 
 enum DType : int { DT_F32 = 0, DT_BF16 = 1, DT_F16 = 2 };
 
@@ -42,6 +46,7 @@ struct ChunkArgs {
     int first, n;       // slot range
     int n_new;          // tokens processed per slot in this launch (<= kMaxNewPerLaunch)
     int j0_cap;         // max over the range of the buffered count j0 (sizes smem)
+    int j_add;          // added to the device count (verify split into several launches)
     int tok_total;      // tokens per slot in the caller's q/k/v/alpha/beta/o arrays
     int tok_offset;     // first token of this launch inside those arrays
     int kind;

@@ -80,7 +80,9 @@ la_status check_config(const la_config *c) {
 void compute_sizes(const la_config *c, la_sizes *s) {
     memset(s, 0, sizeof(*s));
     const size_t R = c->max_slots, Hk = c->n_qk_heads, Hv = c->n_v_heads, d = kD;
-    const int T = std::max(c->chunk + c->max_drafts, c->short_cap);
+    // records per (slot, head), padded to a multiple of 4 so the per-head log
+    // decays can be staged with 16-byte bulk copies
+    const int T = (std::max(c->chunk + c->max_drafts, c->short_cap) + 3) & ~3;
     s->capacity = T;
     s->align = kAlign;
     s->state_bytes = R * Hv * d * d * 4;
@@ -132,15 +134,38 @@ la_status set_device(la_buf *b) {
     return LA_OK;
 }
 
-ChunkArgs chunk_args(la_buf *b, int first, int n, int n_new, int j0_cap, int tok_total,
-                     int tok_offset, int kind, const void *q, const void *k, const void *v,
-                     const float *alpha, const float *beta, float *o) {
-    ChunkArgs a;
-    a.dm = b->dm; a.p = b->p;
-    a.first = first; a.n = n; a.n_new = n_new; a.j0_cap = j0_cap;
-    a.tok_total = tok_total; a.tok_offset = tok_offset; a.kind = kind;
-    a.q = q; a.k = k; a.v = v; a.alpha = alpha; a.beta = beta; a.o = o;
-    return a;
+// Enqueue the chunk-attend kernel for tokens [tok_base, tok_base + n_tok) of
+// per-slot arrays holding tok_total tokens, split into launches of at most
+// max_new_per_launch(g) tokens and kMaxSlotsPerLaunch slots.  Launches of a
+// token split see the earlier tokens as buffered records: the device counter
+// advanced for decode/direct/prefill, an explicit offset (j_add) for verify.
+cudaError_t run_chunk(la_buf *b, int first, int n, int n_tok, int j0_cap, int tok_base, int tok_total,
+                      int kind, const void *q, const void *k, const void *v, const float *alpha,
+                      const float *beta, float *o, cudaStream_t s) {
+    const int mx = max_new_per_launch(b->dm.g);
+    const size_t isz = dt_size(b->cfg.in_dtype);
+    const size_t d = kD;
+    for (int off = 0; off < n_tok; off += mx) {
+        const int m = std::min(mx, n_tok - off);
+        for (int s0 = 0; s0 < n; s0 += kMaxSlotsPerLaunch) {
+            ChunkArgs a;
+            a.dm = b->dm; a.p = b->p;
+            a.first = first + s0; a.n = std::min(kMaxSlotsPerLaunch, n - s0);
+            a.n_new = m; a.j0_cap = j0_cap + off;
+            a.j_add = (kind == CK_VERIFY) ? off : 0;
+            a.tok_total = tok_total; a.tok_offset = tok_base + off; a.kind = kind;
+            const size_t sq = (size_t)s0 * tok_total;          // token rows skipped
+            a.q = static_cast<const char *>(q) + sq * b->dm.Hk * d * isz;
+            a.k = static_cast<const char *>(k) + sq * b->dm.Hk * d * isz;
+            a.v = static_cast<const char *>(v) + sq * b->dm.Hv * d * isz;
+            a.alpha = alpha + sq * b->dm.Hv;
+            a.beta = beta + sq * b->dm.Hv;
+            a.o = o ? o + sq * b->dm.Hv * d : nullptr;
+            cudaError_t e = launch_chunk(a, s, &b->launches);
+            if (e != cudaSuccess) return e;
+        }
+    }
+    return cudaSuccess;
 }
 
 }  // namespace
@@ -233,8 +258,8 @@ la_status la_decode_step(la_buf *b, int32_t first, int32_t n, const void *q, con
     }
     if (n == 0) return LA_OK;
     if ((st = set_device(b)) != LA_OK) return st;
-    ChunkArgs a = chunk_args(b, first, n, 1, j0_cap, 1, 0, CK_DECODE, q, k, v, alpha, beta, o);
-    cudaError_t e = launch_chunk(a, static_cast<cudaStream_t>(stream), &b->launches);
+    cudaError_t e = run_chunk(b, first, n, 1, j0_cap, 0, 1, CK_DECODE, q, k, v, alpha, beta, o,
+                              static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(e, "decode launch");
     for (int r = first; r < first + n; ++r) b->occ[r] += 1;
     return LA_OK;
@@ -288,8 +313,8 @@ la_status la_verify_drafts(la_buf *b, int32_t first, int32_t n, int32_t n_draft,
     }
     if (n == 0) return LA_OK;
     if ((st = set_device(b)) != LA_OK) return st;
-    ChunkArgs a = chunk_args(b, first, n, n_draft, j0_cap, n_draft, 0, CK_VERIFY, q, k, v, alpha, beta, o);
-    cudaError_t e = launch_chunk(a, static_cast<cudaStream_t>(stream), &b->launches);
+    cudaError_t e = run_chunk(b, first, n, n_draft, j0_cap, 0, n_draft, CK_VERIFY, q, k, v, alpha, beta, o,
+                              static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(e, "verify launch");
     for (int r = first; r < first + n; ++r) b->pending[r] = n_draft;
     return LA_OK;
@@ -330,12 +355,9 @@ la_status la_direct_short(la_buf *b, int32_t first, int32_t n, int32_t n_new, co
     }
     if (n == 0) return LA_OK;
     if ((st = set_device(b)) != LA_OK) return st;
-    for (int off = 0; off < n_new; off += kMaxNewPerLaunch) {
-        const int m = std::min(kMaxNewPerLaunch, n_new - off);
-        ChunkArgs a = chunk_args(b, first, n, m, j0_cap + off, n_new, off, CK_DIRECT, q, k, v, alpha, beta, o);
-        cudaError_t e = launch_chunk(a, static_cast<cudaStream_t>(stream), &b->launches);
-        if (e != cudaSuccess) return cuda_fail(e, "direct launch");
-    }
+    cudaError_t e = run_chunk(b, first, n, n_new, j0_cap, 0, n_new, CK_DIRECT, q, k, v, alpha, beta, o,
+                              static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "direct launch");
     for (int r = first; r < first + n; ++r) b->len[r] += n_new;
     return LA_OK;
 }
@@ -357,15 +379,11 @@ la_status la_prefill(la_buf *b, int32_t first, int32_t n, int32_t n_tok, const v
     const int C = b->cfg.chunk;
     for (int c0 = 0; c0 < n_tok; c0 += C) {
         const int cn = std::min(C, n_tok - c0);
-        for (int off = 0; off < cn; off += kMaxNewPerLaunch) {
-            const int m = std::min(kMaxNewPerLaunch, cn - off);
-            ChunkArgs a = chunk_args(b, first, n, m, off, n_tok, c0 + off, CK_PREFILL, q, k, v, alpha, beta, o);
-            cudaError_t e = launch_chunk(a, s, &b->launches);
-            if (e != cudaSuccess) return cuda_fail(e, "prefill chunk launch");
-        }
+        cudaError_t e = run_chunk(b, first, n, cn, 0, c0, n_tok, CK_PREFILL, q, k, v, alpha, beta, o, s);
+        if (e != cudaSuccess) return cuda_fail(e, "prefill chunk launch");
         FoldArgs f;
         f.dm = b->dm; f.p = b->p; f.first = first; f.n = n; f.kind = FK_FORCE; f.nacc = nullptr; f.n_draft = 0;
-        cudaError_t e = launch_fold(f, s, &b->launches);
+        e = launch_fold(f, s, &b->launches);
         if (e != cudaSuccess) return cuda_fail(e, "prefill fold launch");
     }
     return LA_OK;

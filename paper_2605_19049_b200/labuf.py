@@ -189,7 +189,8 @@ class LaBuf:
         nK = c.max_slots * c.n_qk_heads * T * c.d_k
         nU = c.max_slots * c.n_v_heads * T * c.d_v
         K = self._buffer[s.off_k:s.off_k + nK * isz].view(self.in_torch).view(c.max_slots, c.n_qk_heads, T, c.d_k)
-        U = self._buffer[s.off_u:s.off_u + nU * usz].view(udt).view(c.max_slots, c.n_v_heads, T, c.d_v)
+        # u records are tile-major: [R][Hv][d_v/32][T][32]
+        U = self._buffer[s.off_u:s.off_u + nU * usz].view(udt).view(c.max_slots, c.n_v_heads, c.d_v // 32, T, 32)
         G = self._buffer[s.off_g:s.off_g + c.max_slots * c.n_v_heads * T * 4].view(torch.float32).view(
             c.max_slots, c.n_v_heads, T)
         return K, U, G
