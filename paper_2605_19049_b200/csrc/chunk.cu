@@ -1,8 +1,8 @@
 // chunk.cu — kernels (1) buffered decode, (3) parallel draft verification,
 // (4) direct short-context decoding, and the prefill chunk step.
 //
-// All compute, for n_new new tokens t of one request slot r and the g V
-// heads of one QK head, against j0 buffered records (k_i, u_i, G_i):
+// All compute, for n_new new tokens t of one request slot r and one V head
+// (QK head = h / g), against j0 buffered records (k_i, u_i, G_i):
 //
 //   G_t = G_{t-1} + ln alpha_t                  (cumulative log decay, reading Z2)
 //   a_t = S0 k_t,  b_t = S0 q_t                 (one read of the state tile; absent for direct)
@@ -15,80 +15,145 @@
 // P:395-397), and the parallel form P:374-386 with S0 = 0 (direct).
 // New records (k_t, u_t, G_t) are appended at position j0 + t.
 //
-// B200 structure: one light CTA per (d_v tile of ROWS rows x g V heads, QK
-// head, slot).  At entry the lanes of warp 0 issue one bulk copy each
-// (cp.async.bulk -> SASS UBLKCP) for every operand of the CTA — the fp32
-// state tile, the buffered u sub-tiles, key rows and log decays, and the new
-// tokens — onto a single mbarrier, so a CTA's whole working set is in flight
-// at once and several CTAs per SM keep HBM busy.  The CTA then computes from
-// shared memory with one block barrier (before the forward substitution).
+// B200 structure (measured, tools/microbench_bulk.cu): HBM is saturated by
+// many small CTAs that each put their whole working set in flight with a
+// few bulk copies (cp.async.bulk -> SASS UBLKCP) on one mbarrier — 7.4 TB/s
+// even with 1 KB pieces — while a single issuing thread per SM cannot issue
+// small copies fast enough.  So: one CTA of TPC warps per (row-tile group,
+// V head, slot).  At entry its warps issue the copies — the TPC x 32 rows
+// of fp32 state of the head (ONE contiguous copy, 16 KiB per tile), the
+// tiles' u sub-tiles of all buffered records (contiguous by the tile-major U
+// layout), the QK head's key rows, the log decays and the new tokens — and
+// several CTAs per SM overlap one CTA's compute with the others' loads.
+// Compute: warp w owns d_v tile w (32 rows).  (A) Every state row and every
+// key row is reduced against k_t and q_t by 8-lane teams (each lane owns four
+// interleaved 16-byte column chunks: conflict-free, 3 shuffle levels per
+// value); the key rows are shared out over the CTA's warps.  One block
+// barrier.  (B) The forward substitution over the new tokens with one lane
+// per d_v row, and the o / u / record stores.
 #include "device.cuh"
 #include "internal.h"
 
 namespace labuf {
 
+constexpr int kChunkTPC = 2;        // d_v tiles (warps) per CTA for the state kinds
+constexpr int kDirectTPC = 4;       // ... and for direct slots (the key rows dominate)
+
+__host__ __device__ inline uint32_t al128(uint32_t x) { return (x + 127u) & ~127u; }
+
 struct CtaLayout {
     uint32_t S, U, K, Gs, q, k, v, Ck, Cq, av, bv, Gn, Bn, bar, bytes;
 };
 
-__host__ __device__ inline uint32_t al128(uint32_t x) { return (x + 127u) & ~127u; }
-
-__host__ __device__ inline CtaLayout cta_layout(int G, int ROWS, int nt, bool has_state, int jcap,
-                                                int isz, int usz) {
+__host__ __device__ inline CtaLayout cta_layout(int TPC, int nt, bool has_state, int jcap, int isz, int usz) {
     CtaLayout L;
     const int J = jcap + nt;
     uint32_t o = 0;
-    L.S = o;  o = al128(o + (has_state ? (uint32_t)(G * ROWS * kD * 4) : 0u));
-    L.U = o;  o = al128(o + (uint32_t)(G * ROWS * jcap * usz));
+    L.S = o;  o = al128(o + (has_state ? (uint32_t)(TPC * 32 * kD * 4) : 0u));
+    L.U = o;  o = al128(o + (uint32_t)(TPC * 32 * jcap * usz));
     L.K = o;  o = al128(o + (uint32_t)(jcap * kD * isz));
-    L.Gs = o; o = al128(o + (uint32_t)(G * ((jcap + 3) & ~3) * 4));
+    L.Gs = o; o = al128(o + (uint32_t)(((jcap + 3) & ~3) * 4));
     L.q = o;  o = al128(o + (uint32_t)(nt * kD * isz));
     L.k = o;  o = al128(o + (uint32_t)(nt * kD * isz));
-    L.v = o;  o = al128(o + (uint32_t)(nt * G * ROWS * isz));
-    L.Ck = o; o = al128(o + (uint32_t)(G * nt * J * 4));
-    L.Cq = o; o = al128(o + (uint32_t)(G * nt * J * 4));
-    L.av = o; o = al128(o + (uint32_t)(has_state ? G * nt * ROWS * 4 : 0));
-    L.bv = o; o = al128(o + (uint32_t)(has_state ? G * nt * ROWS * 4 : 0));
-    L.Gn = o; o = al128(o + (uint32_t)(G * nt * 4));
-    L.Bn = o; o = al128(o + (uint32_t)(G * nt * 4));
+    L.v = o;  o = al128(o + (uint32_t)(nt * TPC * 32 * isz));
+    L.Ck = o; o = al128(o + (uint32_t)(nt * J * 4));
+    L.Cq = o; o = al128(o + (uint32_t)(nt * J * 4));
+    L.av = o; o = al128(o + (uint32_t)(has_state ? TPC * nt * 32 * 4 : 0));
+    L.bv = o; o = al128(o + (uint32_t)(has_state ? TPC * nt * 32 * 4 : 0));
+    L.Gn = o; o = al128(o + (uint32_t)(nt * 4));
+    L.Bn = o; o = al128(o + (uint32_t)(nt * 4));
     L.bar = o; o += 16;
     L.bytes = al128(o);
     return L;
 }
 
-template <int NT>
-struct MatvecGroups {
-    // rows per reduction group so that 2 * NT * RG values fit one transposed reduction
-    static constexpr int RG = (16 / NT) > 0 ? 16 / NT : 1;
+// ---------------------------------------------------------------- row loads
+// Lane `seg` (0..7) of an 8-lane team owns columns {4 seg + 32 c + e : c, e < 4}
+// of a 128-wide row: four interleaved 16-byte chunks of an fp32 row, so the
+// 8 lanes of a 128-bit shared-memory phase touch 8 consecutive chunks.
+template <typename T>
+__device__ __forceinline__ void load_row4(const T *row, int seg, float4 (&x)[4]) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) x[c] = load4(row + 4 * seg + 32 * c);
+}
+
+// Sum V values over the 8 lanes of a team (xor 1, 2, 4).  V < 8: every lane
+// gets every sum, returned for value index x = seg (lanes seg >= V get -1).
+// V >= 8: transposed butterfly, lane seg ends with the V/8 sums of value
+// indices x = i + (V/8) seg.
+template <int V>
+struct TeamOut {
+    static constexpr int N = V >= 8 ? V / 8 : 1;
 };
+template <int V>
+__device__ __forceinline__ void team_reduce(float (&v)[V], int seg, float (&res)[TeamOut<V>::N],
+                                            int (&xid)[TeamOut<V>::N]) {
+    if constexpr (V < 8) {
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+            float x = v[j];
+            x += __shfl_xor_sync(0xffffffffu, x, 1);
+            x += __shfl_xor_sync(0xffffffffu, x, 2);
+            x += __shfl_xor_sync(0xffffffffu, x, 4);
+            v[j] = x;
+        }
+        float r = 0.f;
+#pragma unroll
+        for (int j = 0; j < V; ++j)
+            if (seg == j) r = v[j];
+        res[0] = r;
+        xid[0] = seg < V ? seg : -1;
+    } else {
+        int n = V;
+#pragma unroll
+        for (int s = 4; s >= 1; s >>= 1) {
+            const bool upper = (seg & s) != 0;
+            const int h = n / 2;
+#pragma unroll
+            for (int i = 0; i < V / 2; ++i) {
+                if (i < h) {
+                    const float send = upper ? v[i] : v[i + h];
+                    const float keep = upper ? v[i + h] : v[i];
+                    v[i] = keep + __shfl_xor_sync(0xffffffffu, send, s);
+                }
+            }
+            n = h;
+        }
+#pragma unroll
+        for (int i = 0; i < V / 8; ++i) {
+            res[i] = v[i];
+            xid[i] = i + (V / 8) * seg;
+        }
+    }
+}
 
-template <typename InT, typename UT, int G, int ROWS, int NT, bool HAS_STATE, int MINB>
-__global__ void __launch_bounds__(256, MINB) chunk_cta_kernel(const ChunkArgs a) {
-    constexpr int NTHR = 256, NWARP = 8;
-    constexpr int GR = G * ROWS;                 // rows of this CTA (flattened over heads)
-    constexpr int SUB = ROWS / kUSub;            // u sub-tiles per head
-    constexpr int RPW = GR / NWARP;              // mat-vec rows per warp
-    constexpr int RG = MatvecGroups<NT>::RG < RPW ? MatvecGroups<NT>::RG : RPW;
-    constexpr int NV = 2 * NT * RG;
-    static_assert(GR <= NTHR, "one thread per (head,row) in the forward substitution");
-    static_assert(RPW % RG == 0, "row grouping");
-    static_assert(G * NT <= 32, "decay scan runs inside one warp");
+template <typename InT, typename UT, int TPC, int NT, bool HAS_STATE, int MINB>
+__global__ void __launch_bounds__(TPC * 32, MINB) chunk_cta_kernel(const ChunkArgs a) {
+    constexpr int NTHR = TPC * 32;
+    constexpr int V = 2 * NT;                    // reduced values per row: (k_t, q_t) dots
+    constexpr int NOUT = TeamOut<V>::N;
+    constexpr bool KQ_REG = NT <= 2;             // k_t, q_t chunks held in registers
+    constexpr int isz = (int)sizeof(InT), usz = (int)sizeof(UT);
+    constexpr int SR = HAS_STATE ? 32 : 0;       // state rows per warp
+    static_assert(NT <= 32, "decay scan runs inside one warp");
 
-    const int tile = blockIdx.x, hk = blockIdx.y, zi = blockIdx.z;
-    const int r = a.first + zi;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int seg = lane & 7, team = lane >> 3;
     const Dims dm = a.dm;
     const int T = dm.T, Hv = dm.Hv, Hk = dm.Hk;
+    const int tg = blockIdx.x, h = blockIdx.y, zi = blockIdx.z;
+    const int r = a.first + zi, hk = h / dm.g;
+    const int tile0 = tg * TPC;                  // first 32-row d_v tile of the CTA
     const int n_new = a.n_new;
     const bool direct = (a.kind == CK_DIRECT);
-    constexpr int isz = (int)sizeof(InT), usz = (int)sizeof(UT);
     const int *cnt = direct ? a.p.len : a.p.occ;
     const int j0 = cnt[r] + a.j_add;
     const int jb = (j0 + 3) & ~3;
+    const int J = j0 + n_new;
     const int Jst = a.j0_cap + NT;               // row stride of Ck/Cq
 
     extern __shared__ __align__(1024) unsigned char smem[];
-    const CtaLayout L = cta_layout(G, ROWS, NT, HAS_STATE, a.j0_cap, isz, usz);
+    const CtaLayout L = cta_layout(TPC, NT, HAS_STATE, a.j0_cap, isz, usz);
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + L.bar);
     const float *S_s = reinterpret_cast<const float *>(smem + L.S);
     const UT *U_s = reinterpret_cast<const UT *>(smem + L.U);
@@ -107,210 +172,219 @@ __global__ void __launch_bounds__(256, MINB) chunk_cta_kernel(const ChunkArgs a)
     const InT *qin = static_cast<const InT *>(a.q);
     const InT *kin = static_cast<const InT *>(a.k);
     const InT *vin = static_cast<const InT *>(a.v);
+    auto tok_of = [&](int t) { return (size_t)zi * a.tok_total + a.tok_offset + t; };
 
-    // ---- 1. warp 0: one bulk copy per lane for every operand of the CTA
-    if (warp == 0) {
-        if (lane == 0) {
-            mbar_init(full, 1);
-            fence_mbar_init();
-            uint32_t total = (HAS_STATE ? (uint32_t)(GR * kD * 4) : 0u) + (uint32_t)(GR * j0 * usz) +
-                             (uint32_t)(j0 * kD * isz) + (j0 ? (uint32_t)(G * jb * 4) : 0u) +
-                             (uint32_t)(n_new * (2 * kD * isz + GR * isz));
-            mbar_arrive_expect_tx(full, total);
-        }
-        __syncwarp();
-        const int nS = HAS_STATE ? G : 0, nU = j0 ? G * SUB : 0, nK = j0 ? 1 : 0, nG = j0 ? G : 0;
-        const int nQ = n_new;
-        const int ncopy = nS + nU + nK + nG + 2 * nQ + nQ * G;
-        unsigned char *sm = smem;
-        for (int c = lane; c < ncopy; c += 32) {
+    // ---- 0. barrier + expected bytes, then every warp issues its share of the copies
+    int ticket = 0;
+    if (tid == 0) {
+        mbar_init(full, 1);
+        fence_mbar_init();
+        const uint32_t total = (HAS_STATE ? (uint32_t)(TPC * 32 * kD * 4) : 0u) + (uint32_t)(TPC * 32 * j0 * usz) +
+                               (uint32_t)(j0 * kD * isz) + (j0 ? (uint32_t)(jb * 4) : 0u) +
+                               (uint32_t)(n_new * (2 * kD * isz + TPC * 32 * isz));
+        mbar_arrive_expect_tx(full, total);
+        // slot counter: every CTA of the slot takes a ticket after reading the
+        // counter; the last one advances it at its end (round trip hidden)
+        if (a.kind != CK_VERIFY) ticket = atomicAdd(&a.p.ticket[r], 1);
+    }
+    // alpha / beta of the new tokens (lane t), in flight with the copies
+    float al_l = 1.f, be_l = 0.f;
+    if (lane < n_new) {
+        al_l = a.alpha[tok_of(lane) * Hv + h];
+        be_l = a.beta[tok_of(lane) * Hv + h];
+    }
+    __syncthreads();
+    {
+        const int nS = HAS_STATE ? 1 : 0, nU = j0 ? TPC : 0, nK = j0 ? 1 : 0, nG = j0 ? 1 : 0;
+        const int ncopy = nS + nU + nK + nG + 3 * n_new;
+        for (int c = warp + TPC * lane; c < ncopy; c += NTHR) {
             int x = c;
             if (x < nS) {
-                bulk_g2s(sm + L.S + (size_t)x * ROWS * kD * 4,
-                         a.p.state + (((size_t)r * Hv + hk * G + x) * kD + (size_t)tile * ROWS) * kD,
-                         ROWS * kD * 4, full);
+                bulk_g2s(smem + L.S, a.p.state + (((size_t)r * Hv + h) * kD + (size_t)tile0 * 32) * kD,
+                         TPC * 32 * kD * 4, full);
                 continue;
             }
             x -= nS;
             if (x < nU) {
-                const int hh = x / SUB, sb = x % SUB;
                 const UT *src = static_cast<const UT *>(a.p.U) +
-                                ((((size_t)r * Hv + hk * G + hh) * (kD / kUSub) + tile * SUB + sb) * T) * kUSub;
-                bulk_g2s(sm + L.U + (size_t)(hh * SUB + sb) * j0 * kUSub * usz, src,
-                         (uint32_t)(j0 * kUSub * usz), full);
+                                ((((size_t)r * Hv + h) * (kD / kUSub) + tile0 + x) * T) * kUSub;
+                bulk_g2s(smem + L.U + (size_t)x * j0 * kUSub * usz, src, (uint32_t)(j0 * kUSub * usz), full);
                 continue;
             }
             x -= nU;
             if (x < nK) {
-                bulk_g2s(sm + L.K, static_cast<const InT *>(a.p.K) + ((size_t)r * Hk + hk) * T * kD,
+                bulk_g2s(smem + L.K, static_cast<const InT *>(a.p.K) + ((size_t)r * Hk + hk) * T * kD,
                          (uint32_t)(j0 * kD * isz), full);
                 continue;
             }
             x -= nK;
             if (x < nG) {
-                bulk_g2s(sm + L.Gs + (size_t)x * jb * 4, a.p.G + ((size_t)r * Hv + hk * G + x) * T,
-                         (uint32_t)(jb * 4), full);
+                bulk_g2s(smem + L.Gs, a.p.G + ((size_t)r * Hv + h) * T, (uint32_t)(jb * 4), full);
                 continue;
             }
             x -= nG;
-            if (x < 2 * nQ) {
-                const int t = x % nQ;
-                const size_t tok = (size_t)zi * a.tok_total + a.tok_offset + t;
-                bulk_g2s(sm + (x < nQ ? L.q : L.k) + (size_t)t * kD * isz,
-                         (x < nQ ? qin : kin) + (tok * Hk + hk) * kD, kD * isz, full);
-                continue;
-            }
-            x -= 2 * nQ;
-            {
-                const int t = x / G, hh = x % G;
-                const size_t tok = (size_t)zi * a.tok_total + a.tok_offset + t;
-                bulk_g2s(sm + L.v + (size_t)(t * G + hh) * ROWS * isz,
-                         vin + (tok * Hv + hk * G + hh) * kD + (size_t)tile * ROWS, ROWS * isz, full);
-            }
+            const int t = x % n_new, kind = x / n_new;
+            if (kind == 0)
+                bulk_g2s(smem + L.q + (size_t)t * kD * isz, qin + (tok_of(t) * Hk + hk) * kD, kD * isz, full);
+            else if (kind == 1)
+                bulk_g2s(smem + L.k + (size_t)t * kD * isz, kin + (tok_of(t) * Hk + hk) * kD, kD * isz, full);
+            else
+                bulk_g2s(smem + L.v + (size_t)t * TPC * 32 * isz, vin + (tok_of(t) * Hv + h) * kD + tile0 * 32,
+                         TPC * 32 * isz, full);
         }
     }
 
-    // ---- 2. every warp: cumulative log decay of the new tokens in registers
-    //         (lane l <-> token t = l / G, head hh = l % G), while the copies fly
-    float gn_l = 0.f, be_l = 0.f;
+    // ---- 1. cumulative log decay of the new tokens in registers (lane t),
+    //         while the copies fly
     unsigned bad = 0;
-    {
-        const bool own = lane < G * n_new;
-        const int hh = lane % G, t = lane / G;
-        float x = 0.f;
-        if (own) {
-            const size_t tok = (size_t)zi * a.tok_total + a.tok_offset + t;
-            const float al = a.alpha[tok * Hv + hk * G + hh];
-            be_l = a.beta[tok * Hv + hk * G + hh];
-            x = logf(al);
-            if (dm.validate) {
-                if (!(al > 0.f && al <= 1.f)) bad |= 0x1u;
-                if (!(be_l >= 0.f && be_l <= 1.f)) bad |= 0x2u;
-            }
-        }
-#pragma unroll
-        for (int off = 1; off < NT; off <<= 1) {
-            const float y = __shfl_up_sync(0xffffffffu, x, off * G);
-            if (lane >= off * G) x += y;
-        }
-        const float g0 = (own && j0 > 0) ? a.p.G[((size_t)r * Hv + hk * G + hh) * T + j0 - 1] : 0.f;
-        gn_l = g0 + x;
-        if (warp == 0 && own) {
-            Gn_s[hh * NT + t] = gn_l;
-            Bn_s[hh * NT + t] = be_l;
+    float x_l = 0.f;
+    if (lane < n_new) {
+        x_l = logf(al_l);
+        if (dm.validate && warp == 0) {
+            if (!(al_l > 0.f && al_l <= 1.f)) bad |= 0x1u;
+            if (!(be_l >= 0.f && be_l <= 1.f)) bad |= 0x2u;
         }
     }
-    // (the block barrier below orders mbarrier init before any other warp waits)
-    __syncthreads();
+#pragma unroll
+    for (int off = 1; off < NT; off <<= 1) {
+        const float y = __shfl_up_sync(0xffffffffu, x_l, off);
+        if (lane >= off) x_l += y;
+    }
     mbar_wait(full, 0);
+    const float gn_l = (j0 > 0 ? G_s[j0 - 1] : 0.f) + x_l;
+    if (warp == 0 && lane < n_new) {
+        Gn_s[lane] = gn_l;
+        Bn_s[lane] = be_l;
+    }
 
-    // ---- 3. key scores -> decay-weighted coefficients (Z3)
-    //   Ck[h][t][i] = e^{G_t-G_i} (k_t . k_i), i <  j0+t ;  Cq: (q_t . k_i), i <= j0+t
+    // ---- 2. rows with 8-lane teams, 4 rows per warp step:
+    //      state rows of the warp's tile: a = S0 k_t, b = S0 q_t;
+    //      key rows i (shared out over the warps):
+    //        Ck[t][i] = e^{G_t-G_i} (k_t.k_i) (i < j0+t),  Cq[t][i] = e^{G_t-G_i} (q_t.k_i) (i <= j0+t)  (Z3)
     {
-        const int J = j0 + n_new;
-        for (int i = warp; i < J; i += NWARP) {
-            const float4 ki = load4((i < j0 ? K_s + (size_t)i * kD : k_s + (size_t)(i - j0) * kD) + 4 * lane);
-            float vals[2 * NT];
+        float4 kx[KQ_REG ? NT : 1][4], qx[KQ_REG ? NT : 1][4];
+        if constexpr (KQ_REG) {
 #pragma unroll
             for (int t = 0; t < NT; ++t) {
-                vals[2 * t] = dot4(ki, load4(k_s + (size_t)t * kD + 4 * lane));
-                vals[2 * t + 1] = dot4(ki, load4(q_s + (size_t)t * kD + 4 * lane));
+                const int tt = t < n_new ? t : 0;
+                load_row4(k_s + (size_t)tt * kD, seg, kx[t]);
+                load_row4(q_s + (size_t)tt * kD, seg, qx[t]);
             }
-            const float red = transposed_reduce<2 * NT>(vals, lane);
-            // lane l holds value (t = l>>1, isq = l&1); weights per head from the scan lanes
+        }
+        const int KS = (J + 3) / 4;                          // key-row steps of the CTA
+        const int my_ks = KS > warp ? (KS - warp + TPC - 1) / TPC : 0;
+        const int nsteps = SR / 4 + my_ks;
+        for (int st = 0; st < nsteps; ++st) {
+            const bool srow = st < SR / 4;                    // warp-uniform
+            const int rf = srow ? st * 4 + team : ((st - SR / 4) * TPC + warp) * 4 + team;
+            float4 x[4];
+            if (srow) {
+                load_row4(S_s + (size_t)(warp * 32 + rf) * kD, seg, x);
+            } else if (rf < J) {
+                load_row4(rf < j0 ? K_s + (size_t)rf * kD : k_s + (size_t)(rf - j0) * kD, seg, x);
+            } else {
 #pragma unroll
-            for (int hh = 0; hh < G; ++hh) {
-                const int t = (lane >> 1) % NT;
-                const float gt = __shfl_sync(0xffffffffu, gn_l, t * G + hh);
-                const float gnew = __shfl_sync(0xffffffffu, gn_l, ((i - j0) > 0 ? (i - j0) : 0) * G + hh);
-                if (lane < 2 * n_new) {
-                    const bool isq = lane & 1;
-                    const bool valid = isq ? (i <= j0 + t) : (i < j0 + t);
-                    float c = 0.f;
-                    if (valid) c = expf(gt - (i < j0 ? G_s[hh * jb + i] : gnew)) * red;
-                    (isq ? Cq : Ck)[(hh * NT + t) * Jst + i] = c;
+                for (int c = 0; c < 4; ++c) x[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+            float vals[V];
+#pragma unroll
+            for (int t = 0; t < NT; ++t) {
+                float pk0 = 0.f, pk1 = 0.f, pq0 = 0.f, pq1 = 0.f;
+#pragma unroll
+                for (int c = 0; c < 4; c += 2) {
+                    float4 k0, k1, q0, q1;
+                    if constexpr (KQ_REG) {
+                        k0 = kx[t][c]; k1 = kx[t][c + 1]; q0 = qx[t][c]; q1 = qx[t][c + 1];
+                    } else {
+                        k0 = load4(k_s + (size_t)t * kD + 4 * seg + 32 * c);
+                        k1 = load4(k_s + (size_t)t * kD + 4 * seg + 32 * (c + 1));
+                        q0 = load4(q_s + (size_t)t * kD + 4 * seg + 32 * c);
+                        q1 = load4(q_s + (size_t)t * kD + 4 * seg + 32 * (c + 1));
+                    }
+                    pk0 += dot4(x[c], k0);
+                    pk1 += dot4(x[c + 1], k1);
+                    pq0 += dot4(x[c], q0);
+                    pq1 += dot4(x[c + 1], q1);
+                }
+                vals[2 * t] = pk0 + pk1;
+                vals[2 * t + 1] = pq0 + pq1;
+            }
+            float res[NOUT];
+            int xid[NOUT];
+            team_reduce<V>(vals, seg, res, xid);
+            if (srow) {
+#pragma unroll
+                for (int o = 0; o < NOUT; ++o) {
+                    const int t = xid[o] >> 1;
+                    if (xid[o] >= 0 && t < n_new) ((xid[o] & 1) ? bv : av)[(warp * NT + t) * 32 + rf] = res[o];
+                }
+            } else {
+                const int i = rf;
+                const int inew = (i - j0) > 0 ? (i - j0) : 0;
+#pragma unroll
+                for (int o = 0; o < NOUT; ++o) {
+                    const int t = xid[o] >= 0 ? (xid[o] >> 1) : 0;
+                    const bool isq = xid[o] & 1;
+                    const float gt = __shfl_sync(0xffffffffu, gn_l, t);
+                    const float gnew = __shfl_sync(0xffffffffu, gn_l, inew < NT ? inew : 0);
+                    if (xid[o] >= 0 && i < J && t < n_new) {
+                        const bool valid = isq ? (i <= j0 + t) : (i < j0 + t);
+                        float cf = 0.f;
+                        if (valid) cf = expf(gt - (i < j0 ? G_s[i] : gnew)) * res[o];
+                        (isq ? Cq : Ck)[t * Jst + i] = cf;
+                    }
                 }
             }
         }
     }
-    // ---- 4. state mat-vecs a_t = S0 k_t, b_t = S0 q_t (transposed warp reduction)
-    if (HAS_STATE) {
-#pragma unroll
-        for (int rg0 = 0; rg0 < RPW; rg0 += RG) {
-            float4 s4[RG];
-#pragma unroll
-            for (int rr = 0; rr < RG; ++rr)
-                s4[rr] = reinterpret_cast<const float4 *>(S_s + (size_t)(warp * RPW + rg0 + rr) * kD)[lane];
-            float vals[NV];
-#pragma unroll
-            for (int t = 0; t < NT; ++t) {
-                const float4 k4 = load4(k_s + (size_t)t * kD + 4 * lane);
-                const float4 q4 = load4(q_s + (size_t)t * kD + 4 * lane);
-#pragma unroll
-                for (int rr = 0; rr < RG; ++rr) {
-                    vals[(rr * NT + t) * 2 + 0] = dot4(s4[rr], k4);
-                    vals[(rr * NT + t) * 2 + 1] = dot4(s4[rr], q4);
-                }
-            }
-            const float red = transposed_reduce<NV>(vals, lane);
-            if (lane < NV) {
-                const int ab = lane & 1, t = (lane >> 1) % NT, rr = (lane >> 1) / NT;
-                const int rf = warp * RPW + rg0 + rr;
-                if (t < n_new) (ab ? bv : av)[((rf / ROWS) * NT + t) * ROWS + rf % ROWS] = red;
-            }
+    if (dm.validate) {
+        for (int e = tid; e < n_new * kD; e += NTHR) {
+            const float kk = to_f(k_s[e]), qq = to_f(q_s[e]);
+            if (!(isfinite(kk) && isfinite(qq))) bad |= 0x4u;
         }
-    }
-    if (dm.validate && tid < n_new * kD) {
-        const float kk = to_f(k_s[tid]), qq = to_f(q_s[tid]);
-        if (!(isfinite(kk) && isfinite(qq))) bad |= 0x4u;
     }
     __syncthreads();
 
-    // ---- 5. slot counter: every CTA of the slot has read it (it did so before
-    //         the barrier above); the last one advances it.  Off the critical
-    //         path (last warp), no fence: the next launch consumes it.
-    if (a.kind != CK_VERIFY && tid == NTHR - 1) {
-        if (atomicAdd(&a.p.ticket[r], 1) == (int)(gridDim.x * gridDim.y) - 1) {
-            a.p.ticket[r] = 0;
-            if (direct) a.p.len[r] = j0 + n_new;
-            else a.p.occ[r] = j0 + n_new;
-        }
-    }
-
-    // ---- 6. forward substitution over the new tokens, one thread per (head, row)
-    if (tid < GR) {
-        const int hh = tid / ROWS, row = tid % ROWS, h = hk * G + hh;
-        const int drow = tile * ROWS + row;
-        const int sb = row / kUSub, rr = row % kUSub;
-        const UT *ut = U_s + (size_t)(hh * SUB + sb) * j0 * kUSub + rr;
-        UT *Uout = static_cast<UT *>(a.p.U) +
-                   ((((size_t)r * Hv + h) * (kD / kUSub) + tile * SUB + sb) * T + j0) * kUSub + rr;
+    // ---- 3. forward substitution over the new tokens, lane = d_v row of the warp's tile
+    {
+        const int row = lane, tile = tile0 + warp;
+        const int drow = tile * 32 + row;
+        const UT *ut = U_s + (size_t)warp * j0 * kUSub + row;
+        UT *Uout = static_cast<UT *>(a.p.U) + ((((size_t)r * Hv + h) * (kD / kUSub) + tile) * T + j0) * kUSub + row;
         float un[NT];
 #pragma unroll
         for (int t = 0; t < NT; ++t) {
             if (t < n_new) {
-                const float *ck = Ck + (hh * NT + t) * Jst;
-                const float *cq = Cq + (hh * NT + t) * Jst;
-                float acc_k = 0.f, acc_q = 0.f;
-#pragma unroll 4
-                for (int i = 0; i < j0; ++i) {
-                    const float ui = to_f(ut[(size_t)i * kUSub]);
-                    acc_k = fmaf(ck[i], ui, acc_k);
-                    acc_q = fmaf(cq[i], ui, acc_q);
+                const float *ck = Ck + t * Jst;
+                const float *cq = Cq + t * Jst;
+                float ak0 = 0.f, ak1 = 0.f, aq0 = 0.f, aq1 = 0.f;
+                int i = 0;
+                for (; i + 1 < j0; i += 2) {
+                    const float u0 = to_f(ut[(size_t)i * kUSub]);
+                    const float u1 = to_f(ut[(size_t)(i + 1) * kUSub]);
+                    ak0 = fmaf(ck[i], u0, ak0);
+                    aq0 = fmaf(cq[i], u0, aq0);
+                    ak1 = fmaf(ck[i + 1], u1, ak1);
+                    aq1 = fmaf(cq[i + 1], u1, aq1);
                 }
+                if (i < j0) {
+                    const float u0 = to_f(ut[(size_t)i * kUSub]);
+                    ak0 = fmaf(ck[i], u0, ak0);
+                    aq0 = fmaf(cq[i], u0, aq0);
+                }
+                float acc_k = ak0 + ak1, acc_q = aq0 + aq1;
 #pragma unroll
                 for (int tp = 0; tp < t; ++tp) {
                     acc_k = fmaf(ck[j0 + tp], un[tp], acc_k);
                     acc_q = fmaf(cq[j0 + tp], un[tp], acc_q);
                 }
-                const size_t tok = (size_t)zi * a.tok_total + a.tok_offset + t;
-                const float vt = to_f(v_s[(t * G + hh) * ROWS + row]);
-                const float bt = Bn_s[hh * NT + t];
-                const float eG = expf(Gn_s[hh * NT + t]);
+                const float vt = to_f(v_s[t * TPC * 32 + warp * 32 + row]);
+                const float bt = Bn_s[t];
+                const float eG = expf(Gn_s[t]);
                 float u, o;
                 if (HAS_STATE) {
-                    u = bt * (vt - fmaf(eG, av[(hh * NT + t) * ROWS + row], acc_k));
-                    o = fmaf(eG, bv[(hh * NT + t) * ROWS + row], acc_q);
+                    u = bt * (vt - fmaf(eG, av[(warp * NT + t) * 32 + row], acc_k));
+                    o = fmaf(eG, bv[(warp * NT + t) * 32 + row], acc_q);
                 } else {
                     u = bt * (vt - acc_k);
                     o = acc_q;
@@ -319,62 +393,58 @@ __global__ void __launch_bounds__(256, MINB) chunk_cta_kernel(const ChunkArgs a)
                 un[t] = to_f(us);                      // the stored (rounded) value
                 o = fmaf(cq[j0 + t], un[t], o);
                 if (dm.validate && !isfinite(vt)) bad |= 0x4u;
-                if (a.o) a.o[(tok * Hv + h) * kD + drow] = o;
+                if (a.o) a.o[(tok_of(t) * Hv + h) * kD + drow] = o;
                 Uout[(size_t)t * kUSub] = us;
                 if (dm.keep_raw) {
                     static_cast<InT *>(a.p.V)[(((size_t)r * Hv + h) * T + j0 + t) * kD + drow] =
-                        v_s[(t * G + hh) * ROWS + row];
+                        v_s[t * TPC * 32 + warp * 32 + row];
                     if (tile == 0 && row == 0) a.p.B[((size_t)r * Hv + h) * T + j0 + t] = bt;
                 }
             }
         }
     }
-    // ---- 7. append k_t and G_t records (tile 0 of each QK head)
-    if (tile == 0) {
-        InT *Kdst = static_cast<InT *>(a.p.K) + (((size_t)r * Hk + hk) * T + j0) * kD;
-        for (int idx = tid; idx < n_new * kD; idx += NTHR) Kdst[idx] = k_s[idx];
-        if (tid < G * n_new) {
-            const int hh = tid / n_new, t = tid % n_new;
-            a.p.G[((size_t)r * Hv + hk * G + hh) * T + j0 + t] = Gn_s[hh * NT + t];
+    // ---- 4. records: k_t once per QK head, G_t per V head (first tile group)
+    if (tg == 0) {
+        if (h % dm.g == 0) {
+            InT *Kdst = static_cast<InT *>(a.p.K) + (((size_t)r * Hk + hk) * T + j0) * kD;
+            for (int idx = tid; idx < n_new * kD; idx += NTHR) Kdst[idx] = k_s[idx];
         }
+        if (tid < n_new) a.p.G[((size_t)r * Hv + h) * T + j0 + tid] = Gn_s[tid];
+    }
+    if (a.kind != CK_VERIFY && tid == 0 && ticket == (int)(gridDim.x * gridDim.y) - 1) {
+        a.p.ticket[r] = 0;
+        if (direct) a.p.len[r] = J;
+        else a.p.occ[r] = J;
     }
     if (bad) atomicOr(a.p.status, bad);
 }
 
 // ---------------------------------------------------------------- launch
-template <typename InT, typename UT, int G, int ROWS, int NT, bool HAS_STATE>
+template <typename InT, typename UT, int TPC, int NT, bool HAS_STATE>
 static cudaError_t launch_cfg(const ChunkArgs &a, cudaStream_t s) {
-    const CtaLayout L = cta_layout(G, ROWS, NT, HAS_STATE, a.j0_cap, sizeof(InT), sizeof(UT));
+    const CtaLayout L = cta_layout(TPC, NT, HAS_STATE, a.j0_cap, sizeof(InT), sizeof(UT));
     if (L.bytes > 227 * 1024) return cudaErrorInvalidConfiguration;
-    constexpr int MINB = NT <= 2 ? 3 : (NT <= 8 ? 2 : 1);
-    auto kfn = chunk_cta_kernel<InT, UT, G, ROWS, NT, HAS_STATE, MINB>;
+    constexpr int MINB = NT <= 2 ? (HAS_STATE ? 12 / TPC : 2) : 1;
+    auto kfn = chunk_cta_kernel<InT, UT, TPC, NT, HAS_STATE, MINB>;
     cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.bytes);
     if (e != cudaSuccess) return e;
-    kfn<<<dim3(kD / ROWS, a.dm.Hk, a.n), 256, L.bytes, s>>>(a);
+    kfn<<<dim3(4 / TPC, a.dm.Hv, a.n), TPC * 32, L.bytes, s>>>(a);
     return cudaGetLastError();
 }
 
-template <typename InT, typename UT, int G, bool HAS_STATE>
+template <typename InT, typename UT, int TPC, bool HAS_STATE>
 static cudaError_t launch_nt(const ChunkArgs &a, cudaStream_t s) {
-    constexpr int ROWS = HAS_STATE ? 32 : (256 / G > kD ? kD : 256 / G);
-    constexpr int NTMAX = 32 / G < 16 ? 32 / G : 16;
-    constexpr int NT8 = NTMAX < 8 ? NTMAX : 8;
-    if (a.n_new == 1) return launch_cfg<InT, UT, G, ROWS, 1, HAS_STATE>(a, s);
-    if (a.n_new <= 2) return launch_cfg<InT, UT, G, ROWS, 2, HAS_STATE>(a, s);
-    if (a.n_new <= 4) return launch_cfg<InT, UT, G, ROWS, 4, HAS_STATE>(a, s);
-    if (a.n_new <= 8) return launch_cfg<InT, UT, G, ROWS, NT8, HAS_STATE>(a, s);
-    return launch_cfg<InT, UT, G, ROWS, NTMAX, HAS_STATE>(a, s);
+    if (a.n_new == 1) return launch_cfg<InT, UT, TPC, 1, HAS_STATE>(a, s);
+    if (a.n_new <= 2) return launch_cfg<InT, UT, TPC, 2, HAS_STATE>(a, s);
+    if (a.n_new <= 4) return launch_cfg<InT, UT, TPC, 4, HAS_STATE>(a, s);
+    if (a.n_new <= 8) return launch_cfg<InT, UT, TPC, 8, HAS_STATE>(a, s);
+    return launch_cfg<InT, UT, TPC, 16, HAS_STATE>(a, s);
 }
 
 template <typename InT, typename UT>
 static cudaError_t launch_t(const ChunkArgs &a, cudaStream_t s) {
-    const bool st = a.kind != CK_DIRECT;
-    switch (a.dm.g) {
-        case 1: return st ? launch_nt<InT, UT, 1, true>(a, s) : launch_nt<InT, UT, 1, false>(a, s);
-        case 2: return st ? launch_nt<InT, UT, 2, true>(a, s) : launch_nt<InT, UT, 2, false>(a, s);
-        case 4: return st ? launch_nt<InT, UT, 4, true>(a, s) : launch_nt<InT, UT, 4, false>(a, s);
-        default: return cudaErrorInvalidValue;
-    }
+    if (a.kind == CK_DIRECT) return launch_nt<InT, UT, kDirectTPC, false>(a, s);
+    return launch_nt<InT, UT, kChunkTPC, true>(a, s);
 }
 
 cudaError_t launch_chunk(const ChunkArgs &a, cudaStream_t s, int64_t *launches) {

@@ -11,8 +11,8 @@ constexpr int kRows = 32;        // d_v rows per V head per recurrent-kernel CTA
 constexpr int kUSub = 32;        // U records are stored tile-major: [R][Hv][d/kUSub][T][kUSub]
 constexpr int kMaxNewPerLaunch = 16;
 constexpr int kMaxSlotsPerLaunch = 4096;
-// new tokens per chunk-kernel launch: the log-decay scan runs in one warp
-inline int max_new_per_launch(int g) { return (32 / g) < kMaxNewPerLaunch ? 32 / g : kMaxNewPerLaunch; }
+// new tokens per chunk-kernel launch (the log-decay scan runs in one warp)
+inline int max_new_per_launch(int /*g*/) { return kMaxNewPerLaunch; }
 
 enum DType : int { DT_F32 = 0, DT_BF16 = 1, DT_F16 = 2 };
 

@@ -12,10 +12,10 @@ timeout 900 python -m pytest tests -m gpu -x -q > $OUT/pytest_gpu.log 2>&1; echo
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke rc=$?" >> $OUT/smoke.log
 timeout 600 python bench.py > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=$?" >> $OUT/bench.err
 if [ "${SKIP_NCU:-0}" != "1" ]; then
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv --log-file $OUT/launches.csv \
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:'chunk_|fold_|recurrent_|decode_' -c 3000 --csv --log-file $OUT/launches.csv \
     python bench.py --steps 2 --warmup 3 --no-cpu > $OUT/ncu_launch_bench.log 2>&1
-for K in chunk_cta_kernel fold_kernel recurrent_step_kernel; do
-  timeout 600 ncu --set full --clock-control none --import-source on -k regex:$K -s 200 -c 2 \
+for K in ${NCU_KERNELS:-chunk_ fold_kernel recurrent_step_kernel}; do
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:$K -s 20 -c 2 \
       -o $OUT/prof_$K python bench.py --steps 2 --warmup 3 --no-rows --no-cpu > $OUT/ncu_$K.log 2>&1
 done
 fi
