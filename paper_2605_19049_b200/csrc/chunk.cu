@@ -26,11 +26,14 @@
 // layout), the QK head's key rows, the log decays and the new tokens — and
 // several CTAs per SM overlap one CTA's compute with the others' loads.
 // Compute: warp w owns d_v tile w (32 rows).  (A) Every state row and every
-// key row is reduced against k_t and q_t by 8-lane teams (each lane owns four
-// interleaved 16-byte column chunks: conflict-free, 3 shuffle levels per
-// value); the key rows are shared out over the CTA's warps.  One block
+// key row is reduced against k_t and q_t by 4-lane teams (8 rows per warp
+// step; each lane owns eight parity-swizzled 16-byte column chunks, so the
+// shared-memory reads are conflict-free; packed FFMA2 dot products; 2 shuffle
+// levels per value); the key rows are shared out over the CTA's warps.  One block
 // barrier.  (B) The forward substitution over the new tokens with one lane
 // per d_v row, and the o / u / record stores.
+#include <cstdlib>
+
 #include "device.cuh"
 #include "internal.h"
 
@@ -62,51 +65,72 @@ __host__ __device__ inline CtaLayout cta_layout(int TPC, int nt, bool has_state,
     L.bv = o; o = al128(o + (uint32_t)(has_state ? TPC * nt * 32 * 4 : 0));
     L.Gn = o; o = al128(o + (uint32_t)(nt * 4));
     L.Bn = o; o = al128(o + (uint32_t)(nt * 4));
-    L.bar = o; o += 16;
+    L.bar = o; o += 32;
     L.bytes = al128(o);
     return L;
 }
 
 // ---------------------------------------------------------------- row loads
-// Lane `seg` (0..7) of an 8-lane team owns columns {4 seg + 32 c + e : c, e < 4}
-// of a 128-wide row: four interleaved 16-byte chunks of an fp32 row, so the
-// 8 lanes of a 128-bit shared-memory phase touch 8 consecutive chunks.
+// A 4-lane team reduces one 128-wide row.  Lane `seg` (0..3) owns the eight
+// 16-byte column chunks ch(c) = seg + 4 (c ^ p), c < 8, where p is the row
+// parity of its team: the two rows read in one 128-bit shared-memory phase
+// (8 lanes) then touch 8 distinct bank groups.  k_t / q_t chunks are held in
+// registers in the same per-lane order, so the pairing is static.
+__device__ __forceinline__ int chunk_of(int seg, int p, int c) { return seg + 4 * (c ^ p); }
+
 template <typename T>
-__device__ __forceinline__ void load_row4(const T *row, int seg, float4 (&x)[4]) {
+__device__ __forceinline__ void load_row8(const T *row, int seg, int p, float4 (&x)[8]) {
 #pragma unroll
-    for (int c = 0; c < 4; ++c) x[c] = load4(row + 4 * seg + 32 * c);
+    for (int c = 0; c < 8; ++c) x[c] = load4(row + 4 * chunk_of(seg, p, c));
 }
 
-// Sum V values over the 8 lanes of a team (xor 1, 2, 4).  V < 8: every lane
-// gets every sum, returned for value index x = seg (lanes seg >= V get -1).
-// V >= 8: transposed butterfly, lane seg ends with the V/8 sums of value
-// indices x = i + (V/8) seg.
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+    uint64_t d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d)
+        : "l"(*reinterpret_cast<uint64_t *>(&a)), "l"(*reinterpret_cast<uint64_t *>(&b)),
+          "l"(*reinterpret_cast<uint64_t *>(&c)));
+    return *reinterpret_cast<float2 *>(&d);
+}
+// sum_c x[c] . y[c] as two packed fp32 accumulators (SASS FFMA2)
+__device__ __forceinline__ float dot8x4(const float4 (&x)[8], const float4 (&y)[8]) {
+    float2 a0 = make_float2(0.f, 0.f), a1 = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+        a0 = ffma2(make_float2(x[c].x, x[c].y), make_float2(y[c].x, y[c].y), a0);
+        a1 = ffma2(make_float2(x[c].z, x[c].w), make_float2(y[c].z, y[c].w), a1);
+    }
+    return (a0.x + a0.y) + (a1.x + a1.y);
+}
+
+// Sum V values over the 4 lanes of a team (xor 1, 2).  V < 4: every lane gets
+// every sum, returned for value index x = seg (lanes seg >= V get -1).
+// V >= 4: transposed butterfly, lane seg ends with the V/4 sums of value
+// indices x = i + (V/4) seg.
 template <int V>
 struct TeamOut {
-    static constexpr int N = V >= 8 ? V / 8 : 1;
+    static constexpr int N = V >= 4 ? V / 4 : 1;
 };
 template <int V>
 __device__ __forceinline__ void team_reduce(float (&v)[V], int seg, float (&res)[TeamOut<V>::N],
                                             int (&xid)[TeamOut<V>::N]) {
-    if constexpr (V < 8) {
+    if constexpr (V < 4) {
 #pragma unroll
         for (int j = 0; j < V; ++j) {
             float x = v[j];
             x += __shfl_xor_sync(0xffffffffu, x, 1);
             x += __shfl_xor_sync(0xffffffffu, x, 2);
-            x += __shfl_xor_sync(0xffffffffu, x, 4);
             v[j] = x;
         }
-        float r = 0.f;
+        float r = v[0];
 #pragma unroll
-        for (int j = 0; j < V; ++j)
+        for (int j = 1; j < V; ++j)
             if (seg == j) r = v[j];
         res[0] = r;
         xid[0] = seg < V ? seg : -1;
     } else {
         int n = V;
 #pragma unroll
-        for (int s = 4; s >= 1; s >>= 1) {
+        for (int s = 2; s >= 1; s >>= 1) {
             const bool upper = (seg & s) != 0;
             const int h = n / 2;
 #pragma unroll
@@ -120,25 +144,27 @@ __device__ __forceinline__ void team_reduce(float (&v)[V], int seg, float (&res)
             n = h;
         }
 #pragma unroll
-        for (int i = 0; i < V / 8; ++i) {
+        for (int i = 0; i < V / 4; ++i) {
             res[i] = v[i];
-            xid[i] = i + (V / 8) * seg;
+            xid[i] = i + (V / 4) * seg;
         }
     }
 }
 
-template <typename InT, typename UT, int TPC, int NT, bool HAS_STATE, int MINB>
-__global__ void __launch_bounds__(TPC * 32, MINB) chunk_cta_kernel(const ChunkArgs a) {
-    constexpr int NTHR = TPC * 32;
+template <typename InT, typename UT, int TPC, int WPT, int NT, bool HAS_STATE, int MINB>
+__global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const ChunkArgs a) {
+    constexpr int NTHR = TPC * WPT * 32;
+    constexpr int RPW = 32 / WPT;                // d_v rows per warp
     constexpr int V = 2 * NT;                    // reduced values per row: (k_t, q_t) dots
     constexpr int NOUT = TeamOut<V>::N;
-    constexpr bool KQ_REG = NT <= 2;             // k_t, q_t chunks held in registers
+    constexpr bool KQ_REG = NT == 1;             // k_t, q_t chunks held in registers
     constexpr int isz = (int)sizeof(InT), usz = (int)sizeof(UT);
     constexpr int SR = HAS_STATE ? 32 : 0;       // state rows per warp
     static_assert(NT <= 32, "decay scan runs inside one warp");
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int seg = lane & 7, team = lane >> 3;
+    const int seg = lane & 3, team = lane >> 2, par = team & 1;
+    const int wt = warp / WPT, half = warp % WPT;  // the warp's d_v tile and row block in it
     const Dims dm = a.dm;
     const int T = dm.T, Hv = dm.Hv, Hk = dm.Hk;
     const int tg = blockIdx.x, h = blockIdx.y, zi = blockIdx.z;
@@ -146,15 +172,13 @@ __global__ void __launch_bounds__(TPC * 32, MINB) chunk_cta_kernel(const ChunkAr
     const int tile0 = tg * TPC;                  // first 32-row d_v tile of the CTA
     const int n_new = a.n_new;
     const bool direct = (a.kind == CK_DIRECT);
-    const int *cnt = direct ? a.p.len : a.p.occ;
-    const int j0 = cnt[r] + a.j_add;
-    const int jb = (j0 + 3) & ~3;
-    const int J = j0 + n_new;
     const int Jst = a.j0_cap + NT;               // row stride of Ck/Cq
 
     extern __shared__ __align__(1024) unsigned char smem[];
     const CtaLayout L = cta_layout(TPC, NT, HAS_STATE, a.j0_cap, isz, usz);
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + L.bar);
+    uint64_t *recs = full + 1;                  // second barrier: the buffered records
+    int *j0_s = reinterpret_cast<int *>(smem + L.bar + 16);
     const float *S_s = reinterpret_cast<const float *>(smem + L.S);
     const UT *U_s = reinterpret_cast<const UT *>(smem + L.U);
     const InT *K_s = reinterpret_cast<const InT *>(smem + L.K);
@@ -174,18 +198,20 @@ __global__ void __launch_bounds__(TPC * 32, MINB) chunk_cta_kernel(const ChunkAr
     const InT *vin = static_cast<const InT *>(a.v);
     auto tok_of = [&](int t) { return (size_t)zi * a.tok_total + a.tok_offset + t; };
 
-    // ---- 0. barrier + expected bytes, then every warp issues its share of the copies
-    int ticket = 0;
+    // ---- 0. Two mbarriers.  `full`: the fixed-size operands (state tiles,
+    //         new tokens), requested at once (thread 0: the state, warp 1:
+    //         q_t, k_t, v_t).  `recs`: the buffered records (U, K, G), which
+    //         need the slot's count j0; thread 0 alone reads it, requests the
+    //         records and publishes j0 through `recs`, then takes the slot
+    //         ticket (every CTA of the slot has read the counter before the
+    //         last ticket is drawn).  The state mat-vecs run while the records
+    //         are still in flight.
+    const uint32_t fixed_bytes = (HAS_STATE ? (uint32_t)(TPC * 32 * kD * 4) : 0u) +
+                                 (uint32_t)(n_new * (2 * kD * isz + TPC * 32 * isz));
     if (tid == 0) {
         mbar_init(full, 1);
+        mbar_init(recs, 1);
         fence_mbar_init();
-        const uint32_t total = (HAS_STATE ? (uint32_t)(TPC * 32 * kD * 4) : 0u) + (uint32_t)(TPC * 32 * j0 * usz) +
-                               (uint32_t)(j0 * kD * isz) + (j0 ? (uint32_t)(jb * 4) : 0u) +
-                               (uint32_t)(n_new * (2 * kD * isz + TPC * 32 * isz));
-        mbar_arrive_expect_tx(full, total);
-        // slot counter: every CTA of the slot takes a ticket after reading the
-        // counter; the last one advances it at its end (round trip hidden)
-        if (a.kind != CK_VERIFY) ticket = atomicAdd(&a.p.ticket[r], 1);
     }
     // alpha / beta of the new tokens (lane t), in flight with the copies
     float al_l = 1.f, be_l = 0.f;
@@ -194,36 +220,33 @@ __global__ void __launch_bounds__(TPC * 32, MINB) chunk_cta_kernel(const ChunkAr
         be_l = a.beta[tok_of(lane) * Hv + h];
     }
     __syncthreads();
-    {
-        const int nS = HAS_STATE ? 1 : 0, nU = j0 ? TPC : 0, nK = j0 ? 1 : 0, nG = j0 ? 1 : 0;
-        const int ncopy = nS + nU + nK + nG + 3 * n_new;
-        for (int c = warp + TPC * lane; c < ncopy; c += NTHR) {
-            int x = c;
-            if (x < nS) {
-                bulk_g2s(smem + L.S, a.p.state + (((size_t)r * Hv + h) * kD + (size_t)tile0 * 32) * kD,
-                         TPC * 32 * kD * 4, full);
-                continue;
-            }
-            x -= nS;
-            if (x < nU) {
-                const UT *src = static_cast<const UT *>(a.p.U) +
-                                ((((size_t)r * Hv + h) * (kD / kUSub) + tile0 + x) * T) * kUSub;
-                bulk_g2s(smem + L.U + (size_t)x * j0 * kUSub * usz, src, (uint32_t)(j0 * kUSub * usz), full);
-                continue;
-            }
-            x -= nU;
-            if (x < nK) {
-                bulk_g2s(smem + L.K, static_cast<const InT *>(a.p.K) + ((size_t)r * Hk + hk) * T * kD,
-                         (uint32_t)(j0 * kD * isz), full);
-                continue;
-            }
-            x -= nK;
-            if (x < nG) {
-                bulk_g2s(smem + L.Gs, a.p.G + ((size_t)r * Hv + h) * T, (uint32_t)(jb * 4), full);
-                continue;
-            }
-            x -= nG;
-            const int t = x % n_new, kind = x / n_new;
+    int ticket = 0;
+    if (tid == 0) {
+        mbar_arrive_expect_tx(full, fixed_bytes);
+        if (HAS_STATE)
+            bulk_g2s(smem + L.S, a.p.state + (((size_t)r * Hv + h) * kD + (size_t)tile0 * 32) * kD,
+                     TPC * 32 * kD * 4, full);
+        const int j0v = (direct ? a.p.len : a.p.occ)[r] + a.j_add;
+        const int jbv = (j0v + 3) & ~3;
+        *j0_s = j0v;
+        mbar_arrive_expect_tx(recs, (uint32_t)(TPC * 32 * j0v * usz) + (uint32_t)(j0v * kD * isz) +
+                                        (j0v ? (uint32_t)(jbv * 4) : 0u));
+        if (j0v) {
+            for (int x = 0; x < TPC; ++x)
+                bulk_g2s(smem + L.U + (size_t)x * j0v * kUSub * usz,
+                         static_cast<const UT *>(a.p.U) + ((((size_t)r * Hv + h) * (kD / kUSub) + tile0 + x) * T) * kUSub,
+                         (uint32_t)(j0v * kUSub * usz), recs);
+            bulk_g2s(smem + L.K, static_cast<const InT *>(a.p.K) + ((size_t)r * Hk + hk) * T * kD,
+                     (uint32_t)(j0v * kD * isz), recs);
+            bulk_g2s(smem + L.Gs, a.p.G + ((size_t)r * Hv + h) * T, (uint32_t)(jbv * 4), recs);
+        }
+        if (a.kind != CK_VERIFY) ticket = atomicAdd(&a.p.ticket[r], 1);
+    } else if (NTHR == 32 || warp == 1) {
+        // new tokens: q_t, k_t rows of the QK head and the tiles' v_t slice
+        // (warp 1's lanes, so they issue in parallel with thread 0)
+        const int c0 = NTHR == 32 ? tid - 1 : lane, cs = NTHR == 32 ? 31 : 32;
+        for (int c = c0; c < 3 * n_new; c += cs) {
+            const int t = c % n_new, kind = c / n_new;
             if (kind == 0)
                 bulk_g2s(smem + L.q + (size_t)t * kD * isz, qin + (tok_of(t) * Hk + hk) * kD, kD * isz, full);
             else if (kind == 1)
@@ -234,8 +257,7 @@ __global__ void __launch_bounds__(TPC * 32, MINB) chunk_cta_kernel(const ChunkAr
         }
     }
 
-    // ---- 1. cumulative log decay of the new tokens in registers (lane t),
-    //         while the copies fly
+    // ---- 1. cumulative log decay increments of the new tokens (lane t), in registers
     unsigned bad = 0;
     float x_l = 0.f;
     if (lane < n_new) {
@@ -251,88 +273,101 @@ __global__ void __launch_bounds__(TPC * 32, MINB) chunk_cta_kernel(const ChunkAr
         if (lane >= off) x_l += y;
     }
     mbar_wait(full, 0);
-    const float gn_l = (j0 > 0 ? G_s[j0 - 1] : 0.f) + x_l;
-    if (warp == 0 && lane < n_new) {
-        Gn_s[lane] = gn_l;
-        Bn_s[lane] = be_l;
+    if (a.dbg & 1) {
+        mbar_wait(recs, 0);
+        if (a.kind != CK_VERIFY && tid == 0 && ticket == (int)(gridDim.x * gridDim.y) - 1) {
+            a.p.ticket[r] = 0;
+            const int Jd = *j0_s + n_new;
+            if (direct) a.p.len[r] = Jd;
+            else a.p.occ[r] = Jd;
+        }
+        return;
     }
 
-    // ---- 2. rows with 8-lane teams, 4 rows per warp step:
+    int j0 = 0, J = 0;
+    float gn_l = 0.f;
+    // ---- 2. rows with 4-lane teams, 8 rows per warp step:
     //      state rows of the warp's tile: a = S0 k_t, b = S0 q_t;
     //      key rows i (shared out over the warps):
     //        Ck[t][i] = e^{G_t-G_i} (k_t.k_i) (i < j0+t),  Cq[t][i] = e^{G_t-G_i} (q_t.k_i) (i <= j0+t)  (Z3)
     {
-        float4 kx[KQ_REG ? NT : 1][4], qx[KQ_REG ? NT : 1][4];
+        float4 kx[KQ_REG ? 8 : 1], qx[KQ_REG ? 8 : 1];
         if constexpr (KQ_REG) {
-#pragma unroll
-            for (int t = 0; t < NT; ++t) {
-                const int tt = t < n_new ? t : 0;
-                load_row4(k_s + (size_t)tt * kD, seg, kx[t]);
-                load_row4(q_s + (size_t)tt * kD, seg, qx[t]);
-            }
+            load_row8(k_s, seg, par, kx);
+            load_row8(q_s, seg, par, qx);
         }
-        const int KS = (J + 3) / 4;                          // key-row steps of the CTA
-        const int my_ks = KS > warp ? (KS - warp + TPC - 1) / TPC : 0;
-        const int nsteps = SR / 4 + my_ks;
-        for (int st = 0; st < nsteps; ++st) {
-            const bool srow = st < SR / 4;                    // warp-uniform
-            const int rf = srow ? st * 4 + team : ((st - SR / 4) * TPC + warp) * 4 + team;
-            float4 x[4];
-            if (srow) {
-                load_row4(S_s + (size_t)(warp * 32 + rf) * kD, seg, x);
-            } else if (rf < J) {
-                load_row4(rf < j0 ? K_s + (size_t)rf * kD : k_s + (size_t)(rf - j0) * kD, seg, x);
+        // dots of row x with k_t and q_t (this lane's 32 columns)
+        auto row_dots = [&](const float4 (&x)[8], float (&vals)[V]) {
+            if constexpr (KQ_REG) {
+                vals[0] = dot8x4(x, kx);
+                vals[1] = dot8x4(x, qx);
             } else {
 #pragma unroll
-                for (int c = 0; c < 4; ++c) x[c] = make_float4(0.f, 0.f, 0.f, 0.f);
-            }
-            float vals[V];
-#pragma unroll
-            for (int t = 0; t < NT; ++t) {
-                float pk0 = 0.f, pk1 = 0.f, pq0 = 0.f, pq1 = 0.f;
-#pragma unroll
-                for (int c = 0; c < 4; c += 2) {
-                    float4 k0, k1, q0, q1;
-                    if constexpr (KQ_REG) {
-                        k0 = kx[t][c]; k1 = kx[t][c + 1]; q0 = qx[t][c]; q1 = qx[t][c + 1];
-                    } else {
-                        k0 = load4(k_s + (size_t)t * kD + 4 * seg + 32 * c);
-                        k1 = load4(k_s + (size_t)t * kD + 4 * seg + 32 * (c + 1));
-                        q0 = load4(q_s + (size_t)t * kD + 4 * seg + 32 * c);
-                        q1 = load4(q_s + (size_t)t * kD + 4 * seg + 32 * (c + 1));
-                    }
-                    pk0 += dot4(x[c], k0);
-                    pk1 += dot4(x[c + 1], k1);
-                    pq0 += dot4(x[c], q0);
-                    pq1 += dot4(x[c + 1], q1);
+                for (int t = 0; t < NT; ++t) {
+                    float4 y[8];
+                    load_row8(k_s + (size_t)t * kD, seg, par, y);
+                    vals[2 * t] = dot8x4(x, y);
+                    load_row8(q_s + (size_t)t * kD, seg, par, y);
+                    vals[2 * t + 1] = dot8x4(x, y);
                 }
-                vals[2 * t] = pk0 + pk1;
-                vals[2 * t + 1] = pq0 + pq1;
             }
-            float res[NOUT];
-            int xid[NOUT];
-            team_reduce<V>(vals, seg, res, xid);
-            if (srow) {
+        };
+        // state rows of the warp's tile: 4 steps of 8 rows
+        if constexpr (HAS_STATE) {
+#pragma unroll(NT == 1 ? 4 : 1)
+            for (int st = 0; st < RPW / 8; ++st) {
+                const int rf = half * RPW + st * 8 + team;
+                float4 x[8];
+                load_row8(S_s + (size_t)(wt * 32 + rf) * kD, seg, par, x);
+                float vals[V];
+                row_dots(x, vals);
+                float res[NOUT];
+                int xid[NOUT];
+                team_reduce<V>(vals, seg, res, xid);
 #pragma unroll
                 for (int o = 0; o < NOUT; ++o) {
                     const int t = xid[o] >> 1;
-                    if (xid[o] >= 0 && t < n_new) ((xid[o] & 1) ? bv : av)[(warp * NT + t) * 32 + rf] = res[o];
+                    if (xid[o] >= 0 && t < n_new) ((xid[o] & 1) ? bv : av)[(wt * NT + t) * 32 + rf] = res[o];
                 }
+            }
+        }
+        // ---- the buffered records: j0, log decays
+        mbar_wait(recs, 0);
+        j0 = *j0_s;
+        J = j0 + n_new;
+        gn_l = (j0 > 0 ? G_s[j0 - 1] : 0.f) + x_l;
+        if (warp == 0 && lane < n_new) {
+            Gn_s[lane] = gn_l;
+            Bn_s[lane] = be_l;
+        }
+        // key rows, shared out over the warps in steps of 8
+        const int KS = (J + 7) / 8;
+        for (int ks = warp; ks < KS; ks += TPC * WPT) {
+            const int i = ks * 8 + team;
+            float4 x[8];
+            if (i < J) {
+                load_row8(i < j0 ? K_s + (size_t)i * kD : k_s + (size_t)(i - j0) * kD, seg, par, x);
             } else {
-                const int i = rf;
-                const int inew = (i - j0) > 0 ? (i - j0) : 0;
 #pragma unroll
-                for (int o = 0; o < NOUT; ++o) {
-                    const int t = xid[o] >= 0 ? (xid[o] >> 1) : 0;
-                    const bool isq = xid[o] & 1;
-                    const float gt = __shfl_sync(0xffffffffu, gn_l, t);
-                    const float gnew = __shfl_sync(0xffffffffu, gn_l, inew < NT ? inew : 0);
-                    if (xid[o] >= 0 && i < J && t < n_new) {
-                        const bool valid = isq ? (i <= j0 + t) : (i < j0 + t);
-                        float cf = 0.f;
-                        if (valid) cf = expf(gt - (i < j0 ? G_s[i] : gnew)) * res[o];
-                        (isq ? Cq : Ck)[t * Jst + i] = cf;
-                    }
+                for (int c = 0; c < 8; ++c) x[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+            float vals[V];
+            row_dots(x, vals);
+            float res[NOUT];
+            int xid[NOUT];
+            team_reduce<V>(vals, seg, res, xid);
+            const int inew = (i - j0) > 0 ? (i - j0) : 0;
+#pragma unroll
+            for (int o = 0; o < NOUT; ++o) {
+                const int t = xid[o] >= 0 ? (xid[o] >> 1) : 0;
+                const bool isq = xid[o] & 1;
+                const float gt = __shfl_sync(0xffffffffu, gn_l, t);
+                const float gnew = __shfl_sync(0xffffffffu, gn_l, inew < NT ? inew : 0);
+                if (xid[o] >= 0 && i < J && t < n_new) {
+                    const bool valid = isq ? (i <= j0 + t) : (i < j0 + t);
+                    float cf = 0.f;
+                    if (valid) cf = expf(gt - (i < j0 ? G_s[i] : gnew)) * res[o];
+                    (isq ? Cq : Ck)[t * Jst + i] = cf;
                 }
             }
         }
@@ -345,11 +380,13 @@ __global__ void __launch_bounds__(TPC * 32, MINB) chunk_cta_kernel(const ChunkAr
     }
     __syncthreads();
 
-    // ---- 3. forward substitution over the new tokens, lane = d_v row of the warp's tile
+    // ---- 3. forward substitution over the new tokens.  Lane -> d_v row
+    //         (half * RPW + lane % RPW) of the warp's tile; the WPT lanes of a
+    //         row split the buffered records by i % WPT and combine by shuffle.
     {
-        const int row = lane, tile = tile0 + warp;
+        const int sub = lane / RPW, row = half * RPW + lane % RPW, tile = tile0 + wt;
         const int drow = tile * 32 + row;
-        const UT *ut = U_s + (size_t)warp * j0 * kUSub + row;
+        const UT *ut = U_s + (size_t)wt * j0 * kUSub + row;
         UT *Uout = static_cast<UT *>(a.p.U) + ((((size_t)r * Hv + h) * (kD / kUSub) + tile) * T + j0) * kUSub + row;
         float un[NT];
 #pragma unroll
@@ -358,14 +395,14 @@ __global__ void __launch_bounds__(TPC * 32, MINB) chunk_cta_kernel(const ChunkAr
                 const float *ck = Ck + t * Jst;
                 const float *cq = Cq + t * Jst;
                 float ak0 = 0.f, ak1 = 0.f, aq0 = 0.f, aq1 = 0.f;
-                int i = 0;
-                for (; i + 1 < j0; i += 2) {
+                int i = sub;
+                for (; i + WPT < j0; i += 2 * WPT) {
                     const float u0 = to_f(ut[(size_t)i * kUSub]);
-                    const float u1 = to_f(ut[(size_t)(i + 1) * kUSub]);
+                    const float u1 = to_f(ut[(size_t)(i + WPT) * kUSub]);
                     ak0 = fmaf(ck[i], u0, ak0);
                     aq0 = fmaf(cq[i], u0, aq0);
-                    ak1 = fmaf(ck[i + 1], u1, ak1);
-                    aq1 = fmaf(cq[i + 1], u1, aq1);
+                    ak1 = fmaf(ck[i + WPT], u1, ak1);
+                    aq1 = fmaf(cq[i + WPT], u1, aq1);
                 }
                 if (i < j0) {
                     const float u0 = to_f(ut[(size_t)i * kUSub]);
@@ -374,17 +411,22 @@ __global__ void __launch_bounds__(TPC * 32, MINB) chunk_cta_kernel(const ChunkAr
                 }
                 float acc_k = ak0 + ak1, acc_q = aq0 + aq1;
 #pragma unroll
+                for (int m = RPW; m < 32; m <<= 1) {
+                    acc_k += __shfl_xor_sync(0xffffffffu, acc_k, m);
+                    acc_q += __shfl_xor_sync(0xffffffffu, acc_q, m);
+                }
+#pragma unroll
                 for (int tp = 0; tp < t; ++tp) {
                     acc_k = fmaf(ck[j0 + tp], un[tp], acc_k);
                     acc_q = fmaf(cq[j0 + tp], un[tp], acc_q);
                 }
-                const float vt = to_f(v_s[t * TPC * 32 + warp * 32 + row]);
+                const float vt = to_f(v_s[t * TPC * 32 + wt * 32 + row]);
                 const float bt = Bn_s[t];
                 const float eG = expf(Gn_s[t]);
                 float u, o;
                 if (HAS_STATE) {
-                    u = bt * (vt - fmaf(eG, av[(warp * NT + t) * 32 + row], acc_k));
-                    o = fmaf(eG, bv[(warp * NT + t) * 32 + row], acc_q);
+                    u = bt * (vt - fmaf(eG, av[(wt * NT + t) * 32 + row], acc_k));
+                    o = fmaf(eG, bv[(wt * NT + t) * 32 + row], acc_q);
                 } else {
                     u = bt * (vt - acc_k);
                     o = acc_q;
@@ -392,13 +434,15 @@ __global__ void __launch_bounds__(TPC * 32, MINB) chunk_cta_kernel(const ChunkAr
                 const UT us = from_f<UT>(u);
                 un[t] = to_f(us);                      // the stored (rounded) value
                 o = fmaf(cq[j0 + t], un[t], o);
-                if (dm.validate && !isfinite(vt)) bad |= 0x4u;
-                if (a.o) a.o[(tok_of(t) * Hv + h) * kD + drow] = o;
-                Uout[(size_t)t * kUSub] = us;
-                if (dm.keep_raw) {
-                    static_cast<InT *>(a.p.V)[(((size_t)r * Hv + h) * T + j0 + t) * kD + drow] =
-                        v_s[t * TPC * 32 + warp * 32 + row];
-                    if (tile == 0 && row == 0) a.p.B[((size_t)r * Hv + h) * T + j0 + t] = bt;
+                if (sub == 0) {
+                    if (dm.validate && !isfinite(vt)) bad |= 0x4u;
+                    if (a.o) a.o[(tok_of(t) * Hv + h) * kD + drow] = o;
+                    Uout[(size_t)t * kUSub] = us;
+                    if (dm.keep_raw) {
+                        static_cast<InT *>(a.p.V)[(((size_t)r * Hv + h) * T + j0 + t) * kD + drow] =
+                            v_s[t * TPC * 32 + wt * 32 + row];
+                        if (tile == 0 && row == 0) a.p.B[((size_t)r * Hv + h) * T + j0 + t] = bt;
+                    }
                 }
             }
         }
@@ -420,35 +464,52 @@ __global__ void __launch_bounds__(TPC * 32, MINB) chunk_cta_kernel(const ChunkAr
 }
 
 // ---------------------------------------------------------------- launch
-template <typename InT, typename UT, int TPC, int NT, bool HAS_STATE>
+template <typename InT, typename UT, int TPC, int WPT, int NT, bool HAS_STATE>
 static cudaError_t launch_cfg(const ChunkArgs &a, cudaStream_t s) {
     const CtaLayout L = cta_layout(TPC, NT, HAS_STATE, a.j0_cap, sizeof(InT), sizeof(UT));
     if (L.bytes > 227 * 1024) return cudaErrorInvalidConfiguration;
-    constexpr int MINB = NT <= 2 ? (HAS_STATE ? 12 / TPC : 2) : 1;
-    auto kfn = chunk_cta_kernel<InT, UT, TPC, NT, HAS_STATE, MINB>;
+    constexpr int MINB = NT <= 2 ? (HAS_STATE ? 12 / (TPC * WPT) : 2) : 1;
+    auto kfn = chunk_cta_kernel<InT, UT, TPC, WPT, NT, HAS_STATE, MINB < 1 ? 1 : MINB>;
     cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.bytes);
     if (e != cudaSuccess) return e;
-    kfn<<<dim3(4 / TPC, a.dm.Hv, a.n), TPC * 32, L.bytes, s>>>(a);
+    kfn<<<dim3(4 / TPC, a.dm.Hv, a.n), TPC * WPT * 32, L.bytes, s>>>(a);
     return cudaGetLastError();
 }
 
-template <typename InT, typename UT, int TPC, bool HAS_STATE>
+template <typename InT, typename UT, int TPC, int WPT, bool HAS_STATE>
 static cudaError_t launch_nt(const ChunkArgs &a, cudaStream_t s) {
-    if (a.n_new == 1) return launch_cfg<InT, UT, TPC, 1, HAS_STATE>(a, s);
-    if (a.n_new <= 2) return launch_cfg<InT, UT, TPC, 2, HAS_STATE>(a, s);
-    if (a.n_new <= 4) return launch_cfg<InT, UT, TPC, 4, HAS_STATE>(a, s);
-    if (a.n_new <= 8) return launch_cfg<InT, UT, TPC, 8, HAS_STATE>(a, s);
-    return launch_cfg<InT, UT, TPC, 16, HAS_STATE>(a, s);
+    if (a.n_new == 1) return launch_cfg<InT, UT, TPC, WPT, 1, HAS_STATE>(a, s);
+    if (a.n_new <= 2) return launch_cfg<InT, UT, TPC, WPT, 2, HAS_STATE>(a, s);
+    if (a.n_new <= 4) return launch_cfg<InT, UT, TPC, WPT, 4, HAS_STATE>(a, s);
+    if (a.n_new <= 8) return launch_cfg<InT, UT, TPC, WPT, 8, HAS_STATE>(a, s);
+    return launch_cfg<InT, UT, TPC, WPT, 16, HAS_STATE>(a, s);
+}
+
+static int env_tpc() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("LABUF_CHUNK_TPC");   // tuning sweeps only
+        v = e ? atoi(e) : 0;
+    }
+    return v;
 }
 
 template <typename InT, typename UT>
 static cudaError_t launch_t(const ChunkArgs &a, cudaStream_t s) {
-    if (a.kind == CK_DIRECT) return launch_nt<InT, UT, kDirectTPC, false>(a, s);
-    return launch_nt<InT, UT, kChunkTPC, true>(a, s);
+    if (a.kind == CK_DIRECT) return launch_nt<InT, UT, kDirectTPC, 1, false>(a, s);
+    switch (env_tpc()) {   // tuning sweeps: 1 = 1 tile x 1 warp, 4 = 4 x 1, 22 = 2 x 2, else 2 tiles x 1 warp
+        case 1: return launch_nt<InT, UT, 1, 1, true>(a, s);
+        case 4: return launch_nt<InT, UT, 4, 1, true>(a, s);
+        case 22: return launch_nt<InT, UT, 2, 2, true>(a, s);
+        default: return launch_nt<InT, UT, kChunkTPC, 1, true>(a, s);
+    }
 }
 
-cudaError_t launch_chunk(const ChunkArgs &a, cudaStream_t s, int64_t *launches) {
-    if (a.n <= 0 || a.n_new <= 0) return cudaSuccess;
+cudaError_t launch_chunk(const ChunkArgs &a_in, cudaStream_t s, int64_t *launches) {
+    if (a_in.n <= 0 || a_in.n_new <= 0) return cudaSuccess;
+    static const int dbg = getenv("LABUF_DEBUG") ? atoi(getenv("LABUF_DEBUG")) : 0;
+    ChunkArgs a = a_in;
+    a.dbg = dbg;
     if (a.n_new > max_new_per_launch(a.dm.g)) return cudaErrorInvalidValue;
     cudaError_t e;
     if (a.dm.in_dt == DT_F32)

@@ -53,6 +53,7 @@ struct ChunkArgs {
     const void *q, *k, *v;
     const float *alpha, *beta;
     float *o;           // may be null (prefill without outputs)
+    int dbg;            // tuning experiments only (LABUF_DEBUG): 1 = skip compute, 2 = skip record copies
 };
 
 enum FoldKind : int {

@@ -1,13 +1,14 @@
 #!/bin/bash
-# Sweep the chunk kernel's consumer groups / ring stages on the headline
-# decode workload (bench.py --no-rows).  Usage: bash tools/sweep_chunk.sh tag
+# Sweep chunk-kernel tuning knobs on the headline decode workload
+# (bench.py --no-rows).  Usage: SWEEP="A=1,B=2 C=3 ..." bash tools/sweep_chunk.sh tag
+# Each sweep item is a comma-separated list of environment assignments.
 TAG=${1:-sweep}
 OUT=gpurun_out/$TAG
 mkdir -p $OUT
-for cfg in ${SWEEP:-"0 0" "2 8" "4 8" "8 8" "4 4" "5 10" "2 4"}; do
-  set -- $cfg
-  LABUF_CHUNK_NG=$1 LABUF_CHUNK_NS=$2 timeout 300 python bench.py --no-rows --no-cpu --steps 20 --warmup 3 > $OUT/b_$1_$2.json 2>$OUT/b_$1_$2.err
-  python - $OUT/b_$1_$2.json "$1 $2" <<'PY' >> $OUT/summary.txt
+for cfg in ${SWEEP:-LABUF_CHUNK_RING=1}; do
+  envs=$(echo "$cfg" | tr ',' ' ')
+  env $envs timeout 300 python bench.py --no-rows --no-cpu --steps 20 --warmup 3 > $OUT/b_$cfg.json 2>$OUT/b_$cfg.err
+  python - $OUT/b_$cfg.json "$cfg" <<'PY' >> $OUT/summary.txt
 import json,sys
 try:
     d=json.load(open(sys.argv[1]))
