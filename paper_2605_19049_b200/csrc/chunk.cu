@@ -159,7 +159,6 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
     constexpr int NOUT = TeamOut<V>::N;
     constexpr bool KQ_REG = NT == 1;             // k_t, q_t chunks held in registers
     constexpr int isz = (int)sizeof(InT), usz = (int)sizeof(UT);
-    constexpr int SR = HAS_STATE ? 32 : 0;       // state rows per warp
     static_assert(NT <= 32, "decay scan runs inside one warp");
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;

@@ -6,97 +6,111 @@
 // len with S0 = 0 (compression of a direct-mode slot into a state).
 // The rank-n update is the one dense contraction of the path:
 //   D[c][j] = sum_i  k_i[c] * (w_i u_i[j]),   M = d_k = 128 (TMEM lanes),
-//   N = 64 (half of d_v per CTA), K = n tokens in chunks of 32,
+//   N = 64 (half of d_v per CTA), K = n tokens in chunks of up to 32,
 // issued as tcgen05.mma.kind::tf32 from K-major SWIZZLE_NONE shared-memory
 // operands with the fp32 accumulator in TMEM.  fp32 accuracy comes from
 // split-TF32 (x = hi + lo): bf16 keys are exact in tf32, so 2 passes
 // (K*Whi + K*Wlo); fp32 keys need 3 (Khi*Whi + Khi*Wlo + Klo*Whi).
-// The S0 half-tile (32 KiB, contiguous) is staged by the bulk-copy engine,
-// the epilogue adds e^{G_last} S0 in shared memory and one bulk store writes
-// S_new back.  The layout of D (lane = key index c) makes both the smem
-// epilogue and the state rows conflict-free.
+//
+// B200 structure: one CTA of 4 warps per (half of d_v, V head, slot).  At
+// entry warp 0 allocates the TMEM accumulator while thread 0 reads the
+// slot's counters and puts the 32 KiB S0 half-tile in flight with one bulk
+// copy; every thread then loads ALL of its key / delta-value operand
+// elements for the chunk in one batch (one memory round trip), converts and
+// splits them into the UMMA layouts in shared memory, and thread 0 issues
+// the MMAs.  The epilogue reads TMEM (lane = key index c, conflict-free in
+// the row-major state tile), adds e^{G_last} S0 in shared memory and one
+// bulk store writes S_new back.  Shared memory is sized from the host-known
+// largest record count, so 4 CTAs share an SM at C = 16.
 #include "device.cuh"
 #include "internal.h"
 
 namespace labuf {
 
 constexpr int kFoldNJ = 64;      // d_v rows per CTA
-constexpr int kFoldKC = 32;      // tokens per MMA staging chunk
+constexpr int kFoldKCMax = 32;   // tokens per MMA staging chunk (max)
 constexpr int kFoldThreads = 128;
 
 struct FoldSmem {
-    size_t S, A, Alo, Bhi, Blo, bar, total;
+    uint32_t S, A, Alo, Bhi, Blo, bar, total;
 };
-__host__ __device__ inline FoldSmem fold_smem_layout(bool fp32_in) {
+__host__ __device__ inline FoldSmem fold_smem_layout(bool fp32_in, int kc) {
     FoldSmem L;
-    size_t o = 0;
-    L.S = o;   o += (size_t)kFoldNJ * kD * 4;            // 32 KiB
-    L.A = o;   o += (size_t)kD * kFoldKC * 4;            // 16 KiB
-    L.Alo = o; o += fp32_in ? (size_t)kD * kFoldKC * 4 : 0;
-    L.Bhi = o; o += (size_t)kFoldNJ * kFoldKC * 4;       // 8 KiB
-    L.Blo = o; o += (size_t)kFoldNJ * kFoldKC * 4;
+    uint32_t o = 0;
+    L.S = o;   o += (uint32_t)kFoldNJ * kD * 4;            // 32 KiB
+    L.A = o;   o += (uint32_t)kD * kc * 4;
+    L.Alo = o; o += fp32_in ? (uint32_t)kD * kc * 4 : 0;
+    L.Bhi = o; o += (uint32_t)kFoldNJ * kc * 4;
+    L.Blo = o; o += (uint32_t)kFoldNJ * kc * 4;
     L.bar = o; o += 64;
     L.total = o;
     return L;
 }
 
-// byte offset of element (row, k) in a K-major SWIZZLE_NONE operand with
-// kFoldKC columns: 8x(16 B) core matrices, K-adjacent at +128 B (LBO),
-// 8-row groups at +kFoldKC*32 B (SBO).
-__device__ __forceinline__ uint32_t kmaj_off(int row, int k) {
-    return (uint32_t)((row >> 3) * (kFoldKC * 32) + (k >> 2) * 128 + (row & 7) * 16 + (k & 3) * 4);
+// byte offset of element (row, k) in a K-major SWIZZLE_NONE operand with kc
+// columns: 8x(16 B) core matrices, K-adjacent at +128 B (LBO), 8-row groups
+// at +kc*32 B (SBO).
+__device__ __forceinline__ uint32_t kmaj_off(int row, int k, int kc) {
+    return (uint32_t)((row >> 3) * (kc * 32) + (k >> 2) * 128 + (row & 7) * 16 + (k & 3) * 4);
 }
 
 template <typename InT, typename UT, bool FP32_IN>
-__global__ void __launch_bounds__(kFoldThreads) fold_kernel(const FoldArgs a) {
+__global__ void __launch_bounds__(kFoldThreads, 4) fold_kernel(const FoldArgs a) {
     const int jh = blockIdx.x, h = blockIdx.y, zi = blockIdx.z;
     const int r = a.first + zi;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int tid = threadIdx.x, warp = tid >> 5;
     const Dims dm = a.dm;
     const int T = dm.T, Hv = dm.Hv;
     const int hk = h / dm.g;
-
-    // ---- which records fold (uniform over all CTAs of the slot)
-    const int mode = a.p.mode[r], occ = a.p.occ[r], len = a.p.len[r];
-    int n = 0;
-    bool zero_s0 = false;
-    if (a.kind == FK_FULL) {
-        n = (mode == 0 && occ == dm.C) ? occ : 0;
-    } else if (a.kind == FK_FORCE) {
-        if (mode == 1) { n = len; zero_s0 = true; } else n = occ;
-    } else {  // FK_COMMIT
-        int na = a.nacc[zi];
-        if (na < 0 || na > a.n_draft) {
-            if (dm.validate && tid == 0) atomicOr(a.p.status, 0x8u);
-            na = na < 0 ? 0 : a.n_draft;
-        }
-        n = occ + na;
-    }
-    if (n == 0) return;   // nothing to fold: state untouched, counters unchanged
+    const int KC = a.kc;                           // staging chunk (multiple of 8, <= 32)
 
     extern __shared__ __align__(1024) unsigned char smem[];
-    const FoldSmem L = fold_smem_layout(FP32_IN);
+    const FoldSmem L = fold_smem_layout(FP32_IN, KC);
     float *S_s = reinterpret_cast<float *>(smem + L.S);
     unsigned char *A = smem + L.A, *Alo = smem + L.Alo, *Bhi = smem + L.Bhi, *Blo = smem + L.Blo;
     uint64_t *bar_ld = reinterpret_cast<uint64_t *>(smem + L.bar);
     uint64_t *bar_mma = bar_ld + 1;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bar_ld + 2);
+    int *meta = reinterpret_cast<int *>(bar_ld + 3);      // n, zero_s0
+    float *state_tile = a.p.state + (((size_t)r * Hv + h) * kD + (size_t)jh * kFoldNJ) * kD;
 
+    // ---- which records fold (uniform over all CTAs of the slot); S0 in flight
     if (warp == 0) tmem_alloc<kFoldNJ>(tmem_slot);
-    if (tid == 0) {
+    if (tid == 32) {
         mbar_init(bar_ld, 1);
         mbar_init(bar_mma, 1);
         fence_mbar_init();
+        const int mode = a.p.mode[r], occ = a.p.occ[r], len = a.p.len[r];
+        int n = 0;
+        bool zero_s0 = false;
+        if (a.kind == FK_FULL) {
+            n = (mode == 0 && occ == dm.C) ? occ : 0;
+        } else if (a.kind == FK_FORCE) {
+            if (mode == 1) { n = len; zero_s0 = true; } else n = occ;
+        } else {  // FK_COMMIT
+            int na = a.nacc[zi];
+            if (na < 0 || na > a.n_draft) {
+                if (dm.validate) atomicOr(a.p.status, 0x8u);
+                na = na < 0 ? 0 : a.n_draft;
+            }
+            n = occ + na;
+        }
+        meta[0] = n;
+        meta[1] = zero_s0;
+        if (n > 0 && !zero_s0) {
+            mbar_arrive_expect_tx(bar_ld, kFoldNJ * kD * 4);
+            bulk_g2s(S_s, state_tile, kFoldNJ * kD * 4, bar_ld);
+        }
     }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    const int n = meta[0];
+    const bool zero_s0 = meta[1] != 0;
     const uint32_t tmem = *tmem_slot;
-
-    float *state_tile = a.p.state + (((size_t)r * Hv + h) * kD + (size_t)jh * kFoldNJ) * kD;
-    if (!zero_s0 && tid == 0) {
-        mbar_arrive_expect_tx(bar_ld, kFoldNJ * kD * 4);
-        bulk_g2s(S_s, state_tile, kFoldNJ * kD * 4, bar_ld);
+    if (n == 0) {   // nothing to fold: state untouched, counters unchanged
+        if (warp == 0) tmem_dealloc<kFoldNJ>(tmem);
+        return;
     }
 
     const InT *Kb = static_cast<const InT *>(a.p.K) + ((size_t)r * dm.Hk + hk) * T * kD;
@@ -106,37 +120,52 @@ __global__ void __launch_bounds__(kFoldThreads) fold_kernel(const FoldArgs a) {
     const float g_last = Gb[n - 1];
     const uint32_t idesc = idesc_tf32(128, kFoldNJ);
     uint32_t mma_phase = 0;
+    // per-thread operand coordinates: A column c = tid (all KC tokens);
+    // B row j = tid % 64, tokens of parity tid / 64
+    const int c = tid, jb = tid % kFoldNJ, ip = tid / kFoldNJ;
+    const int jr = jh * kFoldNJ + jb;
+    const UT *Urow = Ub + (size_t)(jr / kUSub) * T * kUSub + jr % kUSub;
 
-    for (int kc0 = 0; kc0 < n; kc0 += kFoldKC) {
-        const int kn = min(kFoldKC, n - kc0);
+    for (int kc0 = 0; kc0 < n; kc0 += KC) {
+        const int kn = min(KC, n - kc0);
         const int kpad = (kn + 7) & ~7;
         if (kc0 > 0) { mbar_wait(bar_mma, mma_phase); mma_phase ^= 1; }
-        // A = K^T chunk: row c (d_k), column i (token), zero padded to kpad
-        for (int idx = tid; idx < kpad * kD; idx += kFoldThreads) {
-            const int i = idx / kD, c = idx % kD;
-            const float x = (i < kn) ? to_f(Kb[(size_t)(kc0 + i) * kD + c]) : 0.f;
-            const uint32_t off = kmaj_off(c, i);
-            if (FP32_IN) {
-                const float hi = tf32_rna(x);
-                *reinterpret_cast<float *>(A + off) = hi;
-                *reinterpret_cast<float *>(Alo + off) = x - hi;
-            } else {
-                *reinterpret_cast<float *>(A + off) = x;   // bf16 values are exact in tf32
+        // ---- one batch of loads: K^T column c and (w_i u_i)[j] for this chunk
+        float kv[kFoldKCMax], uv[kFoldKCMax / 2], wv[kFoldKCMax / 2];
+#pragma unroll
+        for (int i = 0; i < kFoldKCMax; ++i)
+            kv[i] = (i < kn) ? to_f(Kb[(size_t)(kc0 + i) * kD + c]) : 0.f;
+#pragma unroll
+        for (int q = 0; q < kFoldKCMax / 2; ++q) {
+            const int i = 2 * q + ip;
+            uv[q] = (i < kn) ? to_f(Urow[(size_t)(kc0 + i) * kUSub]) : 0.f;
+            wv[q] = (i < kn) ? Gb[kc0 + i] : g_last;
+        }
+        // ---- A = K^T chunk: row c (d_k), column i (token), zero padded to kpad
+#pragma unroll
+        for (int i = 0; i < kFoldKCMax; ++i) {
+            if (i < kpad) {
+                const uint32_t off = kmaj_off(c, i, KC);
+                if (FP32_IN) {
+                    const float hi = tf32_rna(kv[i]);
+                    *reinterpret_cast<float *>(A + off) = hi;
+                    *reinterpret_cast<float *>(Alo + off) = kv[i] - hi;
+                } else {
+                    *reinterpret_cast<float *>(A + off) = kv[i];   // bf16 values are exact in tf32
+                }
             }
         }
-        // B = (w_i u_i)^T chunk: row j (d_v), column i, split hi + lo
-        for (int idx = tid; idx < kpad * kFoldNJ; idx += kFoldThreads) {
-            const int i = idx / kFoldNJ, j = idx % kFoldNJ;
-            float y = 0.f;
-            if (i < kn) {
-                const float w = expf(g_last - Gb[kc0 + i]);
-                const int jr = jh * kFoldNJ + j;
-                y = w * to_f(Ub[((size_t)(jr / kUSub) * T + kc0 + i) * kUSub + jr % kUSub]);
+        // ---- B = (w_i u_i)^T chunk: row j (d_v), column i, split hi + lo
+#pragma unroll
+        for (int q = 0; q < kFoldKCMax / 2; ++q) {
+            const int i = 2 * q + ip;
+            if (i < kpad) {
+                const float y = (i < kn) ? expf(g_last - wv[q]) * uv[q] : 0.f;
+                const float hi = tf32_rna(y);
+                const uint32_t off = kmaj_off(jb, i, KC);
+                *reinterpret_cast<float *>(Bhi + off) = hi;
+                *reinterpret_cast<float *>(Blo + off) = y - hi;
             }
-            const float hi = tf32_rna(y);
-            const uint32_t off = kmaj_off(j, i);
-            *reinterpret_cast<float *>(Bhi + off) = hi;
-            *reinterpret_cast<float *>(Blo + off) = y - hi;
         }
         fence_proxy_async_smem();
         __syncthreads();
@@ -144,13 +173,13 @@ __global__ void __launch_bounds__(kFoldThreads) fold_kernel(const FoldArgs a) {
             tc_fence_after();
             for (int kk = 0; kk < kpad / 8; ++kk) {
                 const uint32_t koff = kk * 256;   // 8 tf32 = 2 core matrices along K
-                const uint64_t da = umma_desc_noswz(smem_u32(A) + koff, 128, kFoldKC * 32);
-                const uint64_t dbh = umma_desc_noswz(smem_u32(Bhi) + koff, 128, kFoldKC * 32);
-                const uint64_t dbl = umma_desc_noswz(smem_u32(Blo) + koff, 128, kFoldKC * 32);
+                const uint64_t da = umma_desc_noswz(smem_u32(A) + koff, 128, KC * 32);
+                const uint64_t dbh = umma_desc_noswz(smem_u32(Bhi) + koff, 128, KC * 32);
+                const uint64_t dbl = umma_desc_noswz(smem_u32(Blo) + koff, 128, KC * 32);
                 tc_mma_tf32(tmem, da, dbh, idesc, (kc0 > 0 || kk > 0) ? 1u : 0u);
                 tc_mma_tf32(tmem, da, dbl, idesc, 1u);
                 if (FP32_IN) {
-                    const uint64_t dal = umma_desc_noswz(smem_u32(Alo) + koff, 128, kFoldKC * 32);
+                    const uint64_t dal = umma_desc_noswz(smem_u32(Alo) + koff, 128, KC * 32);
                     tc_mma_tf32(tmem, dal, dbh, idesc, 1u);
                 }
             }
@@ -164,7 +193,6 @@ __global__ void __launch_bounds__(kFoldThreads) fold_kernel(const FoldArgs a) {
 
     // ---- epilogue: S_new[j][c] = e^{G_last} S0[j][c] + D[c][j]; thread owns key index c
     const float eG = expf(g_last);
-    const int c = warp * 32 + lane;
 #pragma unroll
     for (int cc = 0; cc < kFoldNJ / 32; ++cc) {
         float v[32];
@@ -181,25 +209,24 @@ __global__ void __launch_bounds__(kFoldThreads) fold_kernel(const FoldArgs a) {
     if (tid == 0) {
         bulk_s2g(state_tile, S_s, kFoldNJ * kD * 4);
         bulk_commit();
-        bulk_wait0();
     }
     if (warp == 0) tmem_dealloc<kFoldNJ>(tmem);
 
     // ---- counters: last CTA of the slot resets the buffer
     if (tid == 0) {
-        __threadfence();
         const int nct = gridDim.x * gridDim.y;
         if (atomicAdd(&a.p.ticket[r], 1) == nct - 1) {
             a.p.ticket[r] = 0;
             a.p.occ[r] = 0;
             if (zero_s0) { a.p.mode[r] = 0; a.p.len[r] = 0; }
         }
+        bulk_wait_read0();   // shared memory must stay live until the store has read it
     }
 }
 
 template <typename InT, typename UT, bool FP32_IN>
 static cudaError_t launch_fold_t(const FoldArgs &a, cudaStream_t s) {
-    const FoldSmem L = fold_smem_layout(FP32_IN);
+    const FoldSmem L = fold_smem_layout(FP32_IN, a.kc);
     auto kfn = fold_kernel<InT, UT, FP32_IN>;
     cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
     if (e != cudaSuccess) return e;
@@ -208,8 +235,13 @@ static cudaError_t launch_fold_t(const FoldArgs &a, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-cudaError_t launch_fold(const FoldArgs &a, cudaStream_t s, int64_t *launches) {
-    if (a.n <= 0) return cudaSuccess;
+cudaError_t launch_fold(const FoldArgs &a_in, cudaStream_t s, int64_t *launches) {
+    if (a_in.n <= 0) return cudaSuccess;
+    FoldArgs a = a_in;
+    // staging chunk: the largest record count of the launch, rounded to the
+    // MMA K granule (8), at most 32 (longer folds loop over chunks)
+    int kc = (a.kcap + 7) & ~7;
+    a.kc = kc < 8 ? 8 : (kc > kFoldKCMax ? kFoldKCMax : kc);
     cudaError_t e;
     if (a.dm.in_dt == DT_F32)
         e = launch_fold_t<float, float, true>(a, s);

@@ -69,6 +69,8 @@ struct FoldArgs {
     int kind;
     const int *nacc;    // FK_COMMIT
     int n_draft;
+    int kcap;           // host bound on the records any slot of the launch folds
+    int kc;             // staging chunk (set by launch_fold)
 };
 
 struct RecArgs {
