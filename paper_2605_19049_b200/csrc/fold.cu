@@ -22,6 +22,8 @@
 // the row-major state tile), adds e^{G_last} S0 in shared memory and one
 // bulk store writes S_new back.  Shared memory is sized from the host-known
 // largest record count, so 4 CTAs share an SM at C = 16.
+#include <cstdlib>
+
 #include "device.cuh"
 #include "internal.h"
 
@@ -74,12 +76,42 @@ __global__ void __launch_bounds__(kFoldThreads, 4) fold_kernel(const FoldArgs a)
     int *meta = reinterpret_cast<int *>(bar_ld + 3);      // n, zero_s0
     float *state_tile = a.p.state + (((size_t)r * Hv + h) * kD + (size_t)jh * kFoldNJ) * kD;
 
+    const InT *Kb = static_cast<const InT *>(a.p.K) + ((size_t)r * dm.Hk + hk) * T * kD;
+    // U is tile-major [R][Hv][d/kUSub][T][kUSub]
+    const UT *Ub = static_cast<const UT *>(a.p.U) + ((size_t)r * Hv + h) * T * kD;
+    const float *Gb = a.p.G + ((size_t)r * Hv + h) * T;
+    // per-thread operand coordinates: A column c = tid (all KC tokens);
+    // B row j = tid % 64, tokens of parity tid / 64
+    const int c = tid, jb = tid % kFoldNJ, ip = tid / kFoldNJ;
+    const int jr = jh * kFoldNJ + jb;
+    const UT *Urow = Ub + (size_t)(jr / kUSub) * T * kUSub + jr % kUSub;
+    // operands of one chunk: K^T column c, u_i[j], G_i — the first chunk is
+    // requested at entry, bounded by the host's record count (in-capacity
+    // reads past a slot's own count are never used)
+    float kv[kFoldKCMax], uv[kFoldKCMax / 2], gv[kFoldKCMax / 2];
+    auto load_chunk = [&](int kc0, int kn) {
+#pragma unroll
+        for (int i = 0; i < kFoldKCMax; ++i)
+            kv[i] = (i < kn) ? to_f(Kb[(size_t)(kc0 + i) * kD + c]) : 0.f;
+#pragma unroll
+        for (int q = 0; q < kFoldKCMax / 2; ++q) {
+            const int i = 2 * q + ip;
+            uv[q] = (i < kn) ? to_f(Urow[(size_t)(kc0 + i) * kUSub]) : 0.f;
+            gv[q] = (i < kn) ? Gb[kc0 + i] : 0.f;
+        }
+    };
+
     // ---- which records fold (uniform over all CTAs of the slot); S0 in flight
+    //      at once when the host mirror says every slot of the range folds
     if (warp == 0) tmem_alloc<kFoldNJ>(tmem_slot);
     if (tid == 32) {
         mbar_init(bar_ld, 1);
         mbar_init(bar_mma, 1);
         fence_mbar_init();
+        if (a.spec) {
+            mbar_arrive_expect_tx(bar_ld, kFoldNJ * kD * 4);
+            bulk_g2s(S_s, state_tile, kFoldNJ * kD * 4, bar_ld);
+        }
         const int mode = a.p.mode[r], occ = a.p.occ[r], len = a.p.len[r];
         int n = 0;
         bool zero_s0 = false;
@@ -97,11 +129,12 @@ __global__ void __launch_bounds__(kFoldThreads, 4) fold_kernel(const FoldArgs a)
         }
         meta[0] = n;
         meta[1] = zero_s0;
-        if (n > 0 && !zero_s0) {
+        if (!a.spec && n > 0 && !zero_s0) {
             mbar_arrive_expect_tx(bar_ld, kFoldNJ * kD * 4);
             bulk_g2s(S_s, state_tile, kFoldNJ * kD * 4, bar_ld);
         }
     }
+    load_chunk(0, min(KC, a.kcap));
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -109,49 +142,36 @@ __global__ void __launch_bounds__(kFoldThreads, 4) fold_kernel(const FoldArgs a)
     const bool zero_s0 = meta[1] != 0;
     const uint32_t tmem = *tmem_slot;
     if (n == 0) {   // nothing to fold: state untouched, counters unchanged
+        if (a.spec) mbar_wait(bar_ld, 0);   // the speculative copy must land before exit
         if (warp == 0) tmem_dealloc<kFoldNJ>(tmem);
         return;
     }
-
-    const InT *Kb = static_cast<const InT *>(a.p.K) + ((size_t)r * dm.Hk + hk) * T * kD;
-    // U is tile-major [R][Hv][d/kUSub][T][kUSub]
-    const UT *Ub = static_cast<const UT *>(a.p.U) + ((size_t)r * Hv + h) * T * kD;
-    const float *Gb = a.p.G + ((size_t)r * Hv + h) * T;
     const float g_last = Gb[n - 1];
     const uint32_t idesc = idesc_tf32(128, kFoldNJ);
     uint32_t mma_phase = 0;
-    // per-thread operand coordinates: A column c = tid (all KC tokens);
-    // B row j = tid % 64, tokens of parity tid / 64
-    const int c = tid, jb = tid % kFoldNJ, ip = tid / kFoldNJ;
-    const int jr = jh * kFoldNJ + jb;
-    const UT *Urow = Ub + (size_t)(jr / kUSub) * T * kUSub + jr % kUSub;
 
     for (int kc0 = 0; kc0 < n; kc0 += KC) {
         const int kn = min(KC, n - kc0);
         const int kpad = (kn + 7) & ~7;
-        if (kc0 > 0) { mbar_wait(bar_mma, mma_phase); mma_phase ^= 1; }
-        // ---- one batch of loads: K^T column c and (w_i u_i)[j] for this chunk
-        float kv[kFoldKCMax], uv[kFoldKCMax / 2], wv[kFoldKCMax / 2];
-#pragma unroll
-        for (int i = 0; i < kFoldKCMax; ++i)
-            kv[i] = (i < kn) ? to_f(Kb[(size_t)(kc0 + i) * kD + c]) : 0.f;
-#pragma unroll
-        for (int q = 0; q < kFoldKCMax / 2; ++q) {
-            const int i = 2 * q + ip;
-            uv[q] = (i < kn) ? to_f(Urow[(size_t)(kc0 + i) * kUSub]) : 0.f;
-            wv[q] = (i < kn) ? Gb[kc0 + i] : g_last;
+        if (kc0 > 0) {
+            mbar_wait(bar_mma, mma_phase);
+            mma_phase ^= 1;
+            load_chunk(kc0, kn);
         }
         // ---- A = K^T chunk: row c (d_k), column i (token), zero padded to kpad
 #pragma unroll
         for (int i = 0; i < kFoldKCMax; ++i) {
             if (i < kpad) {
+                // columns past this slot's count are zero (the speculative
+                // loads may hold other records, even non-finite garbage)
+                const float x = i < kn ? kv[i] : 0.f;
                 const uint32_t off = kmaj_off(c, i, KC);
                 if (FP32_IN) {
-                    const float hi = tf32_rna(kv[i]);
+                    const float hi = tf32_rna(x);
                     *reinterpret_cast<float *>(A + off) = hi;
-                    *reinterpret_cast<float *>(Alo + off) = kv[i] - hi;
+                    *reinterpret_cast<float *>(Alo + off) = x - hi;
                 } else {
-                    *reinterpret_cast<float *>(A + off) = kv[i];   // bf16 values are exact in tf32
+                    *reinterpret_cast<float *>(A + off) = x;   // bf16 values are exact in tf32
                 }
             }
         }
@@ -160,7 +180,7 @@ __global__ void __launch_bounds__(kFoldThreads, 4) fold_kernel(const FoldArgs a)
         for (int q = 0; q < kFoldKCMax / 2; ++q) {
             const int i = 2 * q + ip;
             if (i < kpad) {
-                const float y = (i < kn) ? expf(g_last - wv[q]) * uv[q] : 0.f;
+                const float y = (i < kn) ? expf(g_last - gv[q]) * uv[q] : 0.f;
                 const float hi = tf32_rna(y);
                 const uint32_t off = kmaj_off(jb, i, KC);
                 *reinterpret_cast<float *>(Bhi + off) = hi;
@@ -238,6 +258,8 @@ static cudaError_t launch_fold_t(const FoldArgs &a, cudaStream_t s) {
 cudaError_t launch_fold(const FoldArgs &a_in, cudaStream_t s, int64_t *launches) {
     if (a_in.n <= 0) return cudaSuccess;
     FoldArgs a = a_in;
+    static const int spec_env = getenv("LABUF_FOLD_SPEC") ? atoi(getenv("LABUF_FOLD_SPEC")) : 1;
+    a.spec &= spec_env;
     // staging chunk: the largest record count of the launch, rounded to the
     // MMA K granule (8), at most 32 (longer folds loop over chunks)
     int kc = (a.kcap + 7) & ~7;

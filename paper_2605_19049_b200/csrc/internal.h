@@ -70,6 +70,7 @@ struct FoldArgs {
     const int *nacc;    // FK_COMMIT
     int n_draft;
     int kcap;           // host bound on the records any slot of the launch folds
+    int spec;           // host mirror: every slot of the range folds (issue the state copy at entry)
     int kc;             // staging chunk (set by launch_fold)
 };
 

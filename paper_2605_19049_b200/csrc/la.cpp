@@ -269,7 +269,7 @@ la_status la_flush(la_buf *b, int32_t first, int32_t n, int32_t kind, la_stream 
     la_status st;
     if ((st = check_handle(b)) != LA_OK || (st = check_range(b, first, n)) != LA_OK) return st;
     if (kind != LA_FLUSH_FULL && kind != LA_FLUSH_FORCE) return fail(LA_ERR_INVALID, "bad flush kind");
-    bool any = false;
+    bool any = false, all = true;
     int kcap = 0;
     for (int r = first; r < first + n; ++r) {
         if (b->pending[r]) return fail(LA_ERR_MODE, "slot %d has a pending verify (commit first)", r);
@@ -279,13 +279,14 @@ la_status la_flush(la_buf *b, int32_t first, int32_t n, int32_t kind, la_stream 
         else
             nr = b->mode[r] == LA_MODE_CHUNKWISE ? b->occ[r] : b->len[r];
         any |= nr > 0;
+        all &= nr > 0 && !(kind == LA_FLUSH_FORCE && b->mode[r] == LA_MODE_DIRECT);
         kcap = std::max(kcap, nr);
     }
     if (!any) return LA_OK;   // empty flush is not an error (SPEC flush_and_free)
     if ((st = set_device(b)) != LA_OK) return st;
     FoldArgs a;
     a.dm = b->dm; a.p = b->p; a.first = first; a.n = n;
-    a.kind = kind == LA_FLUSH_FULL ? FK_FULL : FK_FORCE; a.nacc = nullptr; a.n_draft = 0; a.kcap = kcap;
+    a.kind = kind == LA_FLUSH_FULL ? FK_FULL : FK_FORCE; a.nacc = nullptr; a.n_draft = 0; a.kcap = kcap; a.spec = all;
     cudaError_t e = launch_fold(a, static_cast<cudaStream_t>(stream), &b->launches);
     if (e != cudaSuccess) return cuda_fail(e, "flush launch");
     for (int r = first; r < first + n; ++r) {
@@ -339,7 +340,7 @@ la_status la_commit_accepted(la_buf *b, int32_t first, int32_t n, const int32_t 
     a.dm = b->dm; a.p = b->p; a.first = first; a.n = n;
     int occ_max = 0;
     for (int r = first; r < first + n; ++r) occ_max = std::max(occ_max, b->occ[r]);
-    a.kind = FK_COMMIT; a.nacc = n_accepted; a.n_draft = nd; a.kcap = occ_max + nd;
+    a.kind = FK_COMMIT; a.nacc = n_accepted; a.n_draft = nd; a.kcap = occ_max + nd; a.spec = 0;
     cudaError_t e = launch_fold(a, static_cast<cudaStream_t>(stream), &b->launches);
     if (e != cudaSuccess) return cuda_fail(e, "commit launch");
     for (int r = first; r < first + n; ++r) { b->occ[r] = 0; b->pending[r] = 0; }
@@ -389,7 +390,7 @@ la_status la_prefill(la_buf *b, int32_t first, int32_t n, int32_t n_tok, const v
         if (e != cudaSuccess) return cuda_fail(e, "prefill chunk launch");
         FoldArgs f;
         f.dm = b->dm; f.p = b->p; f.first = first; f.n = n; f.kind = FK_FORCE; f.nacc = nullptr; f.n_draft = 0;
-        f.kcap = cn;
+        f.kcap = cn; f.spec = 1;
         e = launch_fold(f, s, &b->launches);
         if (e != cudaSuccess) return cuda_fail(e, "prefill fold launch");
     }
