@@ -126,40 +126,35 @@ def measured_peaks():
 
 
 def ncu_traffic(kernel_key):
-    """DRAM bytes per launch from the committed ncu --set full summary, if any."""
+    """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) of
+    the kernel, from the committed ncu --set full summary (tools/ncu_traffic.py
+    writes profiles/ncu_traffic.json), or None."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if not os.path.exists(path):
         return None
     try:
         with open(path) as f:
-            return json.load(f).get(kernel_key)
+            return json.load(f).get(kernel_key, {}).get("dram_bytes")
     except Exception:
         return None
 
 
-def make_inputs(torch, B, Hk, Hv, n, in_dtype, gen, device):
-    """Seeded synthetic decode inputs with the recipe of synth/ (DESIGN.md
-    'Input recipe'), drawn on the device by torch's generator for speed."""
-    tdt = torch.bfloat16 if in_dtype == "bf16" else torch.float32
+def make_inputs(torch, B, Hk, Hv, n, in_dtype, seed, device):
+    """n decode steps of seeded synthetic inputs (synth.device, DESIGN.md
+    'Input recipe'), drawn on the device; plus an fp32 output buffer each."""
+    import synth.device as sd
     out = []
-    for _ in range(n):
-        q = torch.randn(B, Hk, D, generator=gen, device=device)
-        q = q / q.norm(dim=-1, keepdim=True) / D ** 0.5
-        k = torch.randn(B, Hk, D, generator=gen, device=device)
-        k = k / k.norm(dim=-1, keepdim=True)
-        v = torch.randn(B, Hv, D, generator=gen, device=device)
-        a = 1.0 - 0.1 * torch.rand(B, Hv, generator=gen, device=device)
-        b = torch.sigmoid(torch.randn(B, Hv, generator=gen, device=device))
-        out.append({"q": q.to(tdt).contiguous(), "k": k.to(tdt).contiguous(),
-                    "v": v.to(tdt).contiguous(), "alpha": a.contiguous(), "beta": b.contiguous(),
-                    "o": torch.empty(B, Hv, D, dtype=torch.float32, device=device)})
+    for i in range(n):
+        x = sd.tokens(seed + i, B, 1, Hk, Hv, D, in_dtype=in_dtype, device=device, squeeze=True)
+        x["o"] = torch.empty(B, Hv, D, dtype=torch.float32, device=device)
+        out.append(x)
     return out
 
 
-def fill_states(torch, bufs, gen):
-    for b in bufs:
-        st = b.state
-        st.copy_(torch.randn(st.shape, generator=gen, device=st.device) * (1.0 / (4 * D)) ** 0.5)
+def fill_states(torch, bufs, seed):
+    import synth.device as sd
+    for i, b in enumerate(bufs):
+        b.state.copy_(sd.state0(seed + i, b.cfg.max_slots, b.cfg.n_v_heads, D, device=b.state.device))
 
 
 def timed_graphs(torch, stream, graphs, K, W):
@@ -191,7 +186,7 @@ def capture(torch, stream, fn):
 
 
 # ---------------------------------------------------------------- CPU oracle leg
-def cpu_oracle_sample(target_s=12.0, B=64, Hk=16, Hv=32, seed=1002, max_tok=None):
+def cpu_oracle_sample(target_s=15.0, B=64, Hk=16, Hv=32, seed=1002, max_tok=None):
     """Time the fp64 oracle (the recurrence, as it stands) on host cores on a
     bounded sample of the config-2 workload: B slots x Hv heads x T tokens from
     synthetic 32K-context states.  Returns (tokens/s, cores, sample text)."""
@@ -213,11 +208,14 @@ def cpu_oracle_sample(target_s=12.0, B=64, Hk=16, Hv=32, seed=1002, max_tok=None
         oracle.gdn_run(S0, *args, n_threads=cores)
         return time.perf_counter() - t0
 
-    t1 = run(1)
-    T = max(1, int(target_s / max(t1, 1e-3)))
+    # calibrate: per-call overhead (state copy-in) + per-token cost, then one
+    # run sized to about target_s seconds of CPU work
+    t4, t16 = run(4), run(16)
+    per_tok = max((t16 - t4) / 12, 1e-5)
+    T = max(1, int((target_s - t4 + 4 * per_tok) / per_tok))
     if max_tok:
         T = min(T, max_tok)
-    dt = run(T) if T > 1 else t1
+    dt = run(T)
     return B * T / dt, cores, f"{B} slots x {Hv} V heads x {T} tokens (config 2 shape, fp64 recurrence, {dt:.1f} s)"
 
 
@@ -293,17 +291,14 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
+    from paper_2605_19049_b200 import dp
+
     def max_over_ranks(x):
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        return dp.max_over_ranks(x, device=dev)
 
     B, C, NL, Hk, Hv = args.batch, args.chunk, args.layers, 16, 32
     K, W = args.steps, max(3, args.warmup)
-    gen = torch.Generator(device=dev)
-    gen.manual_seed(args.seed * 1000 + rank)
+    seed0 = args.seed * 1000 + 100 * rank      # per-rank inputs: this rank's shard of the global batch
     clocks = ClockSampler(dev.index if world == 1 else local)
     clocks.start()
     peak, peak_src = measured_peaks()
@@ -315,8 +310,8 @@ def main():
     bufs = [L.LaBuf(cfg, device=dev) for _ in range(NL)]
     for b in bufs:
         b.reset(zero_state=False)
-    fill_states(torch, bufs, gen)
-    inputs = [make_inputs(torch, B, Hk, Hv, NL, args.in_dtype, gen, dev) for _ in range(C)]
+    fill_states(torch, bufs, seed0)
+    inputs = [make_inputs(torch, B, Hk, Hv, NL, args.in_dtype, seed0 + 10 * (t + 1), dev) for t in range(C)]
     stream = torch.cuda.Stream(device=dev)
     torch.cuda.synchronize()
 
@@ -375,6 +370,8 @@ def main():
     dec_gbs = gbs(dec_bytes_per_launch, dec_us)
     step_bytes = NL * (B * sum(lb.decode(j) for j in range(C)) + fl_bytes_per_launch)
     traffic = ncu_traffic("decode")
+    traffic_fl = ncu_traffic("flush")
+    traffic_rec = ncu_traffic("recurrent_step")
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
@@ -400,40 +397,69 @@ def main():
                           "hardware": "4x NVIDIA L40S, TP=4, SGLang v0.5.10 + Triton, FP32 state / FP16 KV (P:12, P:232, P:258, P:266)"},
         "kernels": {
             "decode": {"us_per_launch": dec_us, "bytes_per_launch": dec_bytes_per_launch,
-                       "gbs": dec_gbs, "launches_per_step": dec_launches},
+                       "gbs": dec_gbs, "frac_of_measured": dec_gbs / peak, "launches_per_step": dec_launches,
+                       "share_of_step": dec_ms / (dec_ms + fl_ms), "ncu_dram_bytes_per_launch": traffic},
             "flush": {"us_per_launch": fl_us, "bytes_per_launch": fl_bytes_per_launch,
-                      "gbs": gbs(fl_bytes_per_launch, fl_us), "launches_per_step": fl_launches},
+                      "gbs": gbs(fl_bytes_per_launch, fl_us), "frac_of_measured": gbs(fl_bytes_per_launch, fl_us) / peak,
+                      "launches_per_step": fl_launches, "share_of_step": fl_ms / (dec_ms + fl_ms),
+                      "ncu_dram_bytes_per_launch": traffic_fl},
             "recurrent_step": {"us_per_launch": rec_us, "bytes_per_launch": rec_bytes_per_launch,
-                               "gbs": gbs(rec_bytes_per_launch, rec_us)},
+                               "gbs": gbs(rec_bytes_per_launch, rec_us),
+                               "frac_of_measured": gbs(rec_bytes_per_launch, rec_us) / peak,
+                               "ncu_dram_bytes_per_launch": traffic_rec},
         },
-        "roofline": {"bound": "hbm", "kernel": "chunk_attend_kernel (buffered decode, kernel 1)",
+        "roofline": {"bound": "hbm", "kernel": "chunk_cta_kernel (buffered decode, kernel 1)",
                      "achieved": dec_gbs, "peak": peak, "peak_source": peak_src, "unit": "GB/s",
                      "frac": dec_gbs / peak,
                      "traffic": traffic,
                      "algorithmic_bytes_per_launch": dec_bytes_per_launch,
-                     "note": "bytes = B x mean_j(st + inp + j*rec + o + rec) over occupancies j = 0..C-1"},
+                     "note": "achieved = B x mean_j(st + inp + j*rec + o + rec) over occupancies j = 0..C-1 "
+                             "(DESIGN.md section 6) / mean launch time from CUDA events around the captured decode "
+                             "graph; traffic = ncu dram bytes per launch (profiles/ncu_traffic.json)"},
         "gpu_launches": launches_per_step * K,
     }
 
-    # ---- e2e through the public API with host buffers (pinned), eager launches
+    # ---- e2e through the public API with host buffers: every step copies
+    #      that step's q/k/v/alpha/beta from pinned host memory and every
+    #      output back, on two copy streams that overlap the decode launches
+    #      (per-token events keep each decode behind its own inputs)
     K_e2e = min(K, 10)
-    host_in = [[{k: v.cpu().pin_memory() for k, v in inputs[t][l].items() if k != "o"} for l in range(NL)]
-               for t in range(C)]
+    names = ("q", "k", "v", "alpha", "beta")
+    host_in = [[{k_: inputs[t][l][k_].cpu().pin_memory() for k_ in names} for l in range(NL)] for t in range(C)]
     host_out = [[torch.empty(B, Hv, D, dtype=torch.float32).pin_memory() for _ in range(NL)] for _ in range(C)]
     h2d = sum(v.numel() * v.element_size() for t in range(C) for l in range(NL) for v in host_in[t][l].values())
     d2h = sum(x.numel() * x.element_size() for row in host_out for x in row)
+    h2d_stream = torch.cuda.Stream(device=dev)
+    d2h_stream = torch.cuda.Stream(device=dev)
+    ev_in = [[torch.cuda.Event() for _ in range(NL)] for _ in range(C)]
+    ev_out = [[torch.cuda.Event() for _ in range(NL)] for _ in range(C)]
+    ev_done = [[torch.cuda.Event() for _ in range(NL)] for _ in range(C)]
 
     def e2e_step():
+        for t in range(C):
+            for l in range(NL):
+                dst = inputs[t][l]
+                with torch.cuda.stream(h2d_stream):
+                    h2d_stream.wait_event(ev_out[t][l])          # the previous step's decode read dst
+                    for k_ in names:
+                        dst[k_].copy_(host_in[t][l][k_], non_blocking=True)
+                    ev_in[t][l].record(h2d_stream)
         with torch.cuda.stream(stream):
             for t in range(C):
                 for l, b in enumerate(bufs):
                     dst = inputs[t][l]
-                    for k_, v_ in host_in[t][l].items():
-                        dst[k_].copy_(v_, non_blocking=True)
+                    stream.wait_event(ev_in[t][l])
+                    stream.wait_event(ev_done[t][l])             # the previous step's D2H read dst["o"]
                     b.decode_step(0, dst["q"], dst["k"], dst["v"], dst["alpha"], dst["beta"], dst["o"])
-                    host_out[t][l].copy_(dst["o"], non_blocking=True)
+                    ev_out[t][l].record(stream)
             for b in bufs:
                 b.flush(0, B, L.LA_FLUSH_FULL)
+        with torch.cuda.stream(d2h_stream):
+            for t in range(C):
+                for l in range(NL):
+                    d2h_stream.wait_event(ev_out[t][l])
+                    host_out[t][l].copy_(inputs[t][l]["o"], non_blocking=True)
+                    ev_done[t][l].record(d2h_stream)
 
     for _ in range(2):
         e2e_step()
@@ -446,12 +472,15 @@ def main():
     e2e_us_tok = 1e6 * e2e_s / K_e2e / (C * NL)
     line["e2e"] = {"value": world * B / (e2e_us_tok * 1e-6), "unit": UNIT,
                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                   "steps": K_e2e, "note": "eager la_* calls, pinned H2D of each step's q/k/v/alpha/beta and D2H of every output, wall clock"}
+                   "steps": K_e2e,
+                   "note": "la_* calls through the public binding with pinned host buffers: H2D of every "
+                           "step's q/k/v/alpha/beta and D2H of every output inside the timed region, "
+                           "overlapped with the decode on two copy streams; wall clock, max over ranks"}
 
     # ---- extra rows: verify + commit (config 3) and direct (config 4)
     if not args.no_rows:
         del g_dec, g_fl, g_rec
-        line["rows"] = extra_rows(torch, L, cost, dev, stream, gen, K, W, peak, args)
+        line["rows"] = extra_rows(torch, L, cost, dev, stream, seed0 + 5000, K, W, peak, args)
 
     t_c3 = time.time()
     clocks.stop()
@@ -466,37 +495,33 @@ def main():
         dist.destroy_process_group()
 
 
-def extra_rows(torch, L, cost, dev, stream, gen, K, W, peak, args):
+def extra_rows(torch, L, cost, dev, stream, seed, K, W, peak, args):
+    """Config 3 (verify + commit vs recurrent verify + copy) and config 4
+    (direct decode vs recurrent) at their BASELINE sizes."""
+    import synth.device as sd
     rows = {}
     Hk, Hv = 16, 32
     Kr = max(3, min(K, 20))
     gbs = lambda nbytes, us: nbytes / (us * 1e-6) / 1e9
     # ---------------- config 3: batch 256, 4 drafts, verify + commit vs recurrent verify + copy
-    import numpy as np
-    import synth
     B3, N3, NL3 = 256, 4, 2
     lb = cost.LayerBytes.make(Hk, Hv, D, 2, 4)
     cfg = L.make_config(B3, Hk, Hv, chunk=16, max_drafts=N3)
     bufs = [L.LaBuf(cfg, device=dev) for _ in range(NL3)]
     for b in bufs:
         b.reset(zero_state=False)
-    fill_states(torch, bufs, gen)
-    rc = synth.Recipe(seed=1003)
-    nacc = [torch.from_numpy(synth.n_accepted(rc, np.arange(B3), N3, round_idx=l)).to(dev) for l in range(NL3)]
-    tdt = torch.bfloat16
-    def drafts():
-        q = torch.randn(B3, N3, Hk, D, generator=gen, device=dev)
-        k = torch.randn(B3, N3, Hk, D, generator=gen, device=dev)
-        return {"q": (q / q.norm(dim=-1, keepdim=True) / D ** 0.5).to(tdt),
-                "k": (k / k.norm(dim=-1, keepdim=True)).to(tdt),
-                "v": torch.randn(B3, N3, Hv, D, generator=gen, device=dev).to(tdt),
-                "alpha": 1.0 - 0.1 * torch.rand(B3, N3, Hv, generator=gen, device=dev),
-                "beta": torch.sigmoid(torch.randn(B3, N3, Hv, generator=gen, device=dev)),
-                "o": torch.empty(B3, N3, Hv, D, dtype=torch.float32, device=dev)}
-    xs = [drafts() for _ in range(NL3)]
+    fill_states(torch, bufs, seed)
+    nacc = [sd.n_accepted(seed + 10 + l, B3, N3, device=dev) for l in range(NL3)]
+    xs = []
+    for l in range(NL3):
+        x = sd.tokens(seed + 20 + l, B3, N3, Hk, Hv, D, device=dev)
+        x["o"] = torch.empty(B3, N3, Hv, D, dtype=torch.float32, device=dev)
+        xs.append(x)
+
     def ver():
         for b, x in zip(bufs, xs):
             b.verify_drafts(0, x["q"], x["k"], x["v"], x["alpha"], x["beta"], x["o"])
+
     def com():
         for b, na in zip(bufs, nacc):
             b.commit_accepted(0, na)
@@ -507,9 +532,11 @@ def extra_rows(torch, L, cost, dev, stream, gen, K, W, peak, args):
     ver_bytes = B3 * lb.verify(N3)
     com_bytes = sum(lb.commit(0, int(a)) for na in nacc for a in na.cpu().tolist()) / NL3
     temps = [torch.empty(B3, N3, Hv, D, D, dtype=torch.float32, device=dev) for _ in range(NL3)]
+
     def rver():
         for b, x, tp in zip(bufs, xs, temps):
             b.recurrent_verify(0, x["q"], x["k"], x["v"], x["alpha"], x["beta"], tp, x["o"])
+
     def rcom():
         for b, na, tp in zip(bufs, nacc, temps):
             b.recurrent_commit(0, na, tp)
@@ -517,18 +544,21 @@ def extra_rows(torch, L, cost, dev, stream, gen, K, W, peak, args):
     rtot, (rv_ms, rc_ms) = timed_graphs(torch, stream, [grv, grc], Kr, W)
     rus_round = 1e3 * rtot / Kr / NL3
     v_us = 1e3 * v_ms / Kr / NL3
+    c_us = 1e3 * c_ms / Kr / NL3
     rows["verify_commit"] = {
         "workload": f"config3: batch {B3}, {N3} drafts, p_accept 0.7 (mean n_acc {acc_mean:.2f}), {NL3} layers rotated",
-        "us_per_round": us_round, "verify_us": v_us, "commit_us": 1e3 * c_ms / Kr / NL3,
+        "us_per_round": us_round, "verify_us": v_us, "commit_us": c_us,
         "verify_gbs": gbs(ver_bytes, v_us), "verify_frac_of_measured": gbs(ver_bytes, v_us) / peak,
-        "commit_gbs": gbs(com_bytes, 1e3 * c_ms / Kr / NL3),
+        "commit_gbs": gbs(com_bytes, c_us), "commit_frac_of_measured": gbs(com_bytes, c_us) / peak,
         "recurrent_us_per_round": rus_round,
         "recurrent_verify_gbs": gbs(B3 * lb.recurrent_verify(N3), 1e3 * rv_ms / Kr / NL3),
         "speedup_vs_recurrent": rus_round / us_round,
+        "paper_context": "2.78x at 8 drafts on 4x L40S (P:263); model ((m+1)d+2m)/(3d+4m) = 1.62 at 4 drafts (P:190)",
         "temp_state_bytes_recurrent": B3 * N3 * lb.st,
         "capacity_requests_36_layers_180GB": {
             "recurrent": int(180e9 // (36 * (N3 + 1) * lb.st)),
-            "buffered": int(180e9 // (36 * (lb.st + (16 + N3) * lb.rec))),
+            "buffered": int(180e9 // (36 * (lb.st + bufs[0].sizes.capacity * lb.rec))),
+            "buffered_records_reserved_per_slot": bufs[0].sizes.capacity,
         },
     }
     del gv, gc, grv, grc, temps, bufs, xs
@@ -540,18 +570,15 @@ def extra_rows(torch, L, cost, dev, stream, gen, K, W, peak, args):
     cfg = L.make_config(B4, Hk, Hv, chunk=16, short_cap=128, u_dtype="f16")
     b4 = L.LaBuf(cfg, device=dev)
     lb4 = cost.LayerBytes.make(Hk, Hv, D, 2, 2)
-    def tok(n):
-        q = torch.randn(B4, n, Hk, D, generator=gen, device=dev)
-        k = torch.randn(B4, n, Hk, D, generator=gen, device=dev)
-        return {"q": (q / q.norm(dim=-1, keepdim=True) / D ** 0.5).to(tdt),
-                "k": (k / k.norm(dim=-1, keepdim=True)).to(tdt),
-                "v": torch.randn(B4, n, Hv, D, generator=gen, device=dev).to(tdt),
-                "alpha": 1.0 - 0.1 * torch.rand(B4, n, Hv, generator=gen, device=dev),
-                "beta": torch.sigmoid(torch.randn(B4, n, Hv, generator=gen, device=dev)),
-                "o": torch.empty(B4, n, Hv, D, dtype=torch.float32, device=dev)}
-    pre = tok(L0)
-    steps = [tok(1) for _ in range(NS)]
-    def run_direct(timed):
+    pre = sd.tokens(seed + 30, B4, L0, Hk, Hv, D, device=dev)
+    pre["o"] = torch.empty(B4, L0, Hv, D, dtype=torch.float32, device=dev)
+    steps = []
+    for i in range(NS):
+        x = sd.tokens(seed + 40 + i, B4, 1, Hk, Hv, D, device=dev)
+        x["o"] = torch.empty(B4, 1, Hv, D, dtype=torch.float32, device=dev)
+        steps.append(x)
+
+    def run_direct():
         b4.reset(mode=L.LA_MODE_DIRECT, zero_state=False)
         b4.direct_short(0, pre["q"], pre["k"], pre["v"], pre["alpha"], pre["beta"], pre["o"])
         torch.cuda.synchronize()
@@ -563,8 +590,8 @@ def extra_rows(torch, L, cost, dev, stream, gen, K, W, peak, args):
             e1.record(stream)
         torch.cuda.synchronize()
         return e0.elapsed_time(e1)
-    run_direct(False)
-    d_ms = run_direct(True)
+    run_direct()
+    d_ms = min(run_direct() for _ in range(3))
     d_us = 1e3 * d_ms / NS
     d_bytes = B4 * sum(lb4.direct(L0 + s) for s in range(NS)) / NS
     # recurrent baseline at the same batch and the same tokens
@@ -572,15 +599,17 @@ def extra_rows(torch, L, cost, dev, stream, gen, K, W, peak, args):
     br = L.LaBuf(cfgr, device=dev)
     br.reset(zero_state=True)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    for rep in range(2):
+    sq = [{k: v[:, 0].contiguous() for k, v in x.items()} for x in steps]
+    r_ms = []
+    for rep in range(3):
         with torch.cuda.stream(stream):
             e0.record(stream)
-            for x in steps:
-                br.recurrent_step(0, x["q"][:, 0], x["k"][:, 0], x["v"][:, 0], x["alpha"][:, 0],
-                                  x["beta"][:, 0], x["o"][:, 0].contiguous())
+            for x in sq:
+                br.recurrent_step(0, x["q"], x["k"], x["v"], x["alpha"], x["beta"], x["o"])
             e1.record(stream)
         torch.cuda.synchronize()
-    r_us = 1e3 * e0.elapsed_time(e1) / NS
+        r_ms.append(e0.elapsed_time(e1))
+    r_us = 1e3 * min(r_ms) / NS
     rows["direct"] = {
         "workload": f"config4: batch {B4}, direct KV-only decode from context {L0} to {L0 + NS}, u fp16, no state",
         "us_per_step": d_us, "gbs": gbs(d_bytes, d_us), "frac_of_measured": gbs(d_bytes, d_us) / peak,

@@ -14,9 +14,11 @@ timeout 600 python bench.py > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=
 if [ "${SKIP_NCU:-0}" != "1" ]; then
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:'chunk_|fold_|recurrent_|decode_' -c 3000 --csv --log-file $OUT/launches.csv \
     python bench.py --steps 2 --warmup 3 --no-cpu > $OUT/ncu_launch_bench.log 2>&1
-for K in ${NCU_KERNELS:-chunk_ fold_kernel recurrent_step_kernel}; do
-  timeout 600 ncu --set full --clock-control none --import-source on -k regex:$K -s 20 -c 2 \
+for K in chunk_cta fold_kernel recurrent_step_kernel; do
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:$K -s 20 -c 1 \
       -o $OUT/prof_$K python bench.py --steps 2 --warmup 3 --no-rows --no-cpu > $OUT/ncu_$K.log 2>&1
 done
+python tools/ncu_traffic.py $OUT decode=$OUT/prof_chunk_cta.ncu-rep flush=$OUT/prof_fold_kernel.ncu-rep \
+    recurrent_step=$OUT/prof_recurrent_step_kernel.ncu-rep > $OUT/ncu_traffic.log 2>&1
 fi
 ls -la $OUT
