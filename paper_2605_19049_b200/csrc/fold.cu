@@ -29,21 +29,20 @@
 
 namespace labuf {
 
-constexpr int kFoldNJ = 64;      // d_v rows per CTA
 constexpr int kFoldKCMax = 32;   // tokens per MMA staging chunk (max)
 constexpr int kFoldThreads = 128;
 
 struct FoldSmem {
     uint32_t S, A, Alo, Bhi, Blo, bar, total;
 };
-__host__ __device__ inline FoldSmem fold_smem_layout(bool fp32_in, int kc) {
+__host__ __device__ inline FoldSmem fold_smem_layout(bool fp32_in, int nj, int kc) {
     FoldSmem L;
     uint32_t o = 0;
-    L.S = o;   o += (uint32_t)kFoldNJ * kD * 4;            // 32 KiB
+    L.S = o;   o += (uint32_t)nj * kD * 4;                 // nj state rows
     L.A = o;   o += (uint32_t)kD * kc * 4;
     L.Alo = o; o += fp32_in ? (uint32_t)kD * kc * 4 : 0;
-    L.Bhi = o; o += (uint32_t)kFoldNJ * kc * 4;
-    L.Blo = o; o += (uint32_t)kFoldNJ * kc * 4;
+    L.Bhi = o; o += (uint32_t)nj * kc * 4;
+    L.Blo = o; o += (uint32_t)nj * kc * 4;
     L.bar = o; o += 64;
     L.total = o;
     return L;
@@ -56,8 +55,9 @@ __device__ __forceinline__ uint32_t kmaj_off(int row, int k, int kc) {
     return (uint32_t)((row >> 3) * (kc * 32) + (k >> 2) * 128 + (row & 7) * 16 + (k & 3) * 4);
 }
 
-template <typename InT, typename UT, bool FP32_IN>
-__global__ void __launch_bounds__(kFoldThreads, 4) fold_kernel(const FoldArgs a) {
+template <typename InT, typename UT, bool FP32_IN, int kFoldNJ, int KCM>
+__global__ void __launch_bounds__(kFoldThreads, kFoldNJ == 32 && KCM == 16 ? 8 : 4) fold_kernel(const FoldArgs a) {
+    constexpr int NPAR = kFoldThreads / kFoldNJ;   // token parities per B row
     const int jh = blockIdx.x, h = blockIdx.y, zi = blockIdx.z;
     const int r = a.first + zi;
     const int tid = threadIdx.x, warp = tid >> 5;
@@ -67,7 +67,7 @@ __global__ void __launch_bounds__(kFoldThreads, 4) fold_kernel(const FoldArgs a)
     const int KC = a.kc;                           // staging chunk (multiple of 8, <= 32)
 
     extern __shared__ __align__(1024) unsigned char smem[];
-    const FoldSmem L = fold_smem_layout(FP32_IN, KC);
+    const FoldSmem L = fold_smem_layout(FP32_IN, kFoldNJ, KC);
     float *S_s = reinterpret_cast<float *>(smem + L.S);
     unsigned char *A = smem + L.A, *Alo = smem + L.Alo, *Bhi = smem + L.Bhi, *Blo = smem + L.Blo;
     uint64_t *bar_ld = reinterpret_cast<uint64_t *>(smem + L.bar);
@@ -81,21 +81,21 @@ __global__ void __launch_bounds__(kFoldThreads, 4) fold_kernel(const FoldArgs a)
     const UT *Ub = static_cast<const UT *>(a.p.U) + ((size_t)r * Hv + h) * T * kD;
     const float *Gb = a.p.G + ((size_t)r * Hv + h) * T;
     // per-thread operand coordinates: A column c = tid (all KC tokens);
-    // B row j = tid % 64, tokens of parity tid / 64
+    // B row j = tid % NJ, tokens i = ip (mod NPAR)
     const int c = tid, jb = tid % kFoldNJ, ip = tid / kFoldNJ;
     const int jr = jh * kFoldNJ + jb;
     const UT *Urow = Ub + (size_t)(jr / kUSub) * T * kUSub + jr % kUSub;
     // operands of one chunk: K^T column c, u_i[j], G_i — the first chunk is
     // requested at entry, bounded by the host's record count (in-capacity
     // reads past a slot's own count are never used)
-    float kv[kFoldKCMax], uv[kFoldKCMax / 2], gv[kFoldKCMax / 2];
+    float kv[KCM], uv[KCM / NPAR], gv[KCM / NPAR];
     auto load_chunk = [&](int kc0, int kn) {
 #pragma unroll
-        for (int i = 0; i < kFoldKCMax; ++i)
+        for (int i = 0; i < KCM; ++i)
             kv[i] = (i < kn) ? to_f(Kb[(size_t)(kc0 + i) * kD + c]) : 0.f;
 #pragma unroll
-        for (int q = 0; q < kFoldKCMax / 2; ++q) {
-            const int i = 2 * q + ip;
+        for (int q = 0; q < KCM / NPAR; ++q) {
+            const int i = NPAR * q + ip;
             uv[q] = (i < kn) ? to_f(Urow[(size_t)(kc0 + i) * kUSub]) : 0.f;
             gv[q] = (i < kn) ? Gb[kc0 + i] : 0.f;
         }
@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(kFoldThreads, 4) fold_kernel(const FoldArgs a)
         }
         // ---- A = K^T chunk: row c (d_k), column i (token), zero padded to kpad
 #pragma unroll
-        for (int i = 0; i < kFoldKCMax; ++i) {
+        for (int i = 0; i < KCM; ++i) {
             if (i < kpad) {
                 // columns past this slot's count are zero (the speculative
                 // loads may hold other records, even non-finite garbage)
@@ -177,8 +177,8 @@ __global__ void __launch_bounds__(kFoldThreads, 4) fold_kernel(const FoldArgs a)
         }
         // ---- B = (w_i u_i)^T chunk: row j (d_v), column i, split hi + lo
 #pragma unroll
-        for (int q = 0; q < kFoldKCMax / 2; ++q) {
-            const int i = 2 * q + ip;
+        for (int q = 0; q < KCM / NPAR; ++q) {
+            const int i = NPAR * q + ip;
             if (i < kpad) {
                 const float y = (i < kn) ? expf(g_last - gv[q]) * uv[q] : 0.f;
                 const float hi = tf32_rna(y);
@@ -244,15 +244,26 @@ __global__ void __launch_bounds__(kFoldThreads, 4) fold_kernel(const FoldArgs a)
     }
 }
 
-template <typename InT, typename UT, bool FP32_IN>
-static cudaError_t launch_fold_t(const FoldArgs &a, cudaStream_t s) {
-    const FoldSmem L = fold_smem_layout(FP32_IN, a.kc);
-    auto kfn = fold_kernel<InT, UT, FP32_IN>;
+template <typename InT, typename UT, bool FP32_IN, int NJ, int KCM>
+static cudaError_t launch_fold_cfg(const FoldArgs &a, cudaStream_t s) {
+    const FoldSmem L = fold_smem_layout(FP32_IN, NJ, a.kc);
+    auto kfn = fold_kernel<InT, UT, FP32_IN, NJ, KCM>;
     cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
     if (e != cudaSuccess) return e;
-    dim3 grid(kD / kFoldNJ, a.dm.Hv, a.n);
+    dim3 grid(kD / NJ, a.dm.Hv, a.n);
     kfn<<<grid, kFoldThreads, L.total, s>>>(a);
     return cudaGetLastError();
+}
+
+template <typename InT, typename UT, bool FP32_IN>
+static cudaError_t launch_fold_t(const FoldArgs &a, cudaStream_t s) {
+    // LABUF_FOLD_NJ: d_v rows per CTA (32 or 64; tuning sweeps)
+    static const int nj = getenv("LABUF_FOLD_NJ") ? atoi(getenv("LABUF_FOLD_NJ")) : 32;
+    if (nj == 64)
+        return a.kc <= 16 ? launch_fold_cfg<InT, UT, FP32_IN, 64, 16>(a, s)
+                          : launch_fold_cfg<InT, UT, FP32_IN, 64, 32>(a, s);
+    return a.kc <= 16 ? launch_fold_cfg<InT, UT, FP32_IN, 32, 16>(a, s)
+                      : launch_fold_cfg<InT, UT, FP32_IN, 32, 32>(a, s);
 }
 
 cudaError_t launch_fold(const FoldArgs &a_in, cudaStream_t s, int64_t *launches) {
