@@ -45,7 +45,7 @@ constexpr int kDirectTPC = 4;       // ... and for direct slots (the key rows do
 __host__ __device__ inline uint32_t al128(uint32_t x) { return (x + 127u) & ~127u; }
 
 struct CtaLayout {
-    uint32_t S, U, K, Gs, q, k, v, Ck, Cq, av, bv, Gn, Bn, bar, bytes;
+    uint32_t S, U, K, Gs, q, k, v, kq32, Ck, Cq, av, bv, Gn, Bn, bar, bytes;
 };
 
 __host__ __device__ inline CtaLayout cta_layout(int TPC, int nt, bool has_state, int jcap, int isz, int usz) {
@@ -59,6 +59,7 @@ __host__ __device__ inline CtaLayout cta_layout(int TPC, int nt, bool has_state,
     L.q = o;  o = al128(o + (uint32_t)(nt * kD * isz));
     L.k = o;  o = al128(o + (uint32_t)(nt * kD * isz));
     L.v = o;  o = al128(o + (uint32_t)(nt * TPC * 32 * isz));
+    L.kq32 = o; o = al128(o + (nt > 1 && isz == 2 ? (uint32_t)(nt * 2 * kD * 4) : 0u));   // fp32 k_t, q_t
     L.Ck = o; o = al128(o + (uint32_t)(nt * J * 4));
     L.Cq = o; o = al128(o + (uint32_t)(nt * J * 4));
     L.av = o; o = al128(o + (uint32_t)(has_state ? TPC * nt * 32 * 4 : 0));
@@ -283,6 +284,18 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
         return;
     }
 
+    // multi-token launches read k_t / q_t once per row step: widen them to
+    // fp32 once per CTA ([t][k | q][128])
+    constexpr bool KQ32 = !KQ_REG && isz == 2;
+    float *kq32 = reinterpret_cast<float *>(smem + L.kq32);
+    if constexpr (KQ32) {
+        for (int e = tid; e < n_new * kD; e += NTHR) {
+            const int t = e / kD, c = e % kD;
+            kq32[(t * 2 + 0) * kD + c] = to_f(k_s[e]);
+            kq32[(t * 2 + 1) * kD + c] = to_f(q_s[e]);
+        }
+        __syncthreads();
+    }
     int j0 = 0, J = 0;
     float gn_l = 0.f;
     // ---- 2. rows with 4-lane teams, 8 rows per warp step:
@@ -304,9 +317,11 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
 #pragma unroll
                 for (int t = 0; t < NT; ++t) {
                     float4 y[8];
-                    load_row8(k_s + (size_t)t * kD, seg, par, y);
+                    if constexpr (KQ32) load_row8(kq32 + (size_t)(t * 2) * kD, seg, par, y);
+                    else load_row8(k_s + (size_t)t * kD, seg, par, y);
                     vals[2 * t] = dot8x4(x, y);
-                    load_row8(q_s + (size_t)t * kD, seg, par, y);
+                    if constexpr (KQ32) load_row8(kq32 + (size_t)(t * 2 + 1) * kD, seg, par, y);
+                    else load_row8(q_s + (size_t)t * kD, seg, par, y);
                     vals[2 * t + 1] = dot8x4(x, y);
                 }
             }

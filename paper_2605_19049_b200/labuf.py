@@ -13,7 +13,9 @@ from dataclasses import dataclass
 import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "liblabuf.so")
+# LABUF_LIB: an alternative build of the same library (A/B timing of two
+# builds on one box, tools/ab.sh); the default is the in-tree build.
+LIB_PATH = os.environ.get("LABUF_LIB", os.path.join(_PKG, "liblabuf.so"))
 
 LA_OK, LA_ERR_INVALID, LA_ERR_UNSUPPORTED, LA_ERR_CAPACITY, LA_ERR_MODE, LA_ERR_CUDA, LA_ERR_NCCL = range(7)
 LA_DT_F32, LA_DT_BF16, LA_DT_F16 = 0, 1, 2
