@@ -503,6 +503,49 @@ def extra_rows(torch, L, cost, dev, stream, seed, K, W, peak, args):
     Hk, Hv = 16, 32
     Kr = max(3, min(K, 20))
     gbs = lambda nbytes, us: nbytes / (us * 1e-6) / 1e9
+    # ---------------- config 2, flush mode ii (LA_FLUSH_RAW): u recomputed in the
+    #                  flush by the UT transform from the raw records (keep_raw)
+    B2, C2, NL2 = args.batch, args.chunk, 4
+    in_b = 2 if args.in_dtype == "bf16" else 4
+    lb2 = cost.LayerBytes.make(Hk, Hv, D, in_b, 4)
+    cfg = L.make_config(B2, Hk, Hv, chunk=C2, in_dtype=args.in_dtype, keep_raw=True)
+    bufs = [L.LaBuf(cfg, device=dev) for _ in range(NL2)]
+    for b in bufs:
+        b.reset(zero_state=False)
+    fill_states(torch, bufs, seed + 1)
+    xs2 = [make_inputs(torch, B2, Hk, Hv, NL2, args.in_dtype, seed + 2 + t, dev) for t in range(C2)]
+
+    def dec2():
+        for t in range(C2):
+            for b, x in zip(bufs, xs2[t]):
+                b.decode_step(0, x["q"], x["k"], x["v"], x["alpha"], x["beta"], x["o"])
+
+    def fl2(kind):
+        def f():
+            for b in bufs:
+                b.flush(0, B2, kind)
+        return f
+    gd2 = capture(torch, stream, dec2)
+    gr2 = capture(torch, stream, fl2(L.LA_FLUSH_FULL | L.LA_FLUSH_RAW))
+    _, (_, raw_ms) = timed_graphs(torch, stream, [gd2, gr2], Kr, W)
+    gd2b = capture(torch, stream, dec2)      # the host mirror follows captures: one cycle each
+    gi2 = capture(torch, stream, fl2(L.LA_FLUSH_FULL))
+    _, (_, ui_ms) = timed_graphs(torch, stream, [gd2b, gi2], Kr, W)
+    raw_us = 1e3 * raw_ms / Kr / NL2
+    ui_us = 1e3 * ui_ms / Kr / NL2
+    raw_bytes = B2 * (2 * lb2.st + C2 * (Hk * D * in_b + Hv * D * in_b + 8 * Hv))
+    rows["flush_mode_ii"] = {
+        "workload": f"config2: batch {B2}, C={C2}, keep_raw records, {NL2} layers rotated",
+        "us_per_launch": raw_us, "bytes_per_launch": raw_bytes,
+        "gbs": gbs(raw_bytes, raw_us), "frac_of_measured": gbs(raw_bytes, raw_us) / peak,
+        "mode_i_us_per_launch_same_buffers": ui_us,
+        "note": "UT transform in the flush: W = K S0^T and the Gram matrix on CUDA cores, C x C forward "
+                "substitution in shared memory, then the split-TF32 tcgen05 fold (P:392-399, reading Z4)",
+    }
+    del gd2, gr2, gd2b, gi2, bufs, xs2
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+
     # ---------------- config 3: batch 256, 4 drafts, verify + commit vs recurrent verify + copy
     B3, N3, NL3 = 256, 4, 2
     lb = cost.LayerBytes.make(Hk, Hv, D, 2, 4)

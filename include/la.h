@@ -84,8 +84,16 @@ typedef enum { LA_DT_F32 = 0, LA_DT_BF16 = 1, LA_DT_F16 = 2 } la_dtype;
 typedef enum { LA_MODE_CHUNKWISE = 0, LA_MODE_DIRECT = 1 } la_mode;
 typedef enum {
     LA_FLUSH_FULL = 0,   /* fold only slots whose buffer holds `chunk` records */
-    LA_FLUSH_FORCE = 1   /* fold every non-empty slot; a DIRECT slot is compressed
+    LA_FLUSH_FORCE = 1,  /* fold every non-empty slot; a DIRECT slot is compressed
                             into a fresh state and switches to CHUNKWISE */
+    LA_FLUSH_RAW = 2     /* flag, OR-ed into FULL/FORCE: mode ii.  The delta values
+                            are recomputed from the raw records (k, v, beta, G) and
+                            S0 by the UT transform -- W = K S0^T, the n x n forward
+                            substitution T = [I + strictLower(Diag(beta)(Gamma (.)
+                            K K^T))]^{-1}, U = T Diag(beta)(V - Diag(e^G) W)
+                            (K~ as corrected by reading Z4) -- then
+                            folded as in mode i.  Needs keep_raw = 1, else
+                            LA_ERR_INVALID. */
 } la_flush_kind;
 
 /* Device status bits (la_device_status), set only when config.validate = 1. */
@@ -146,7 +154,8 @@ LA_API la_status la_decode_step(la_buf *buf, int32_t first, int32_t n, const voi
 
 /* Flush, kernel (2): S <- e^{G_last} S0 +
  * sum_{i<occ} e^{G_last-G_i} u_i k_i^T on the 5th-gen tensor cores
- * (tcgen05, split-TF32, accumulator in TMEM), occ <- 0.  FULL folds slots
+ * (tcgen05, split-TF32, accumulator in TMEM), occ <- 0.  kind may carry
+ * LA_FLUSH_RAW (mode ii: u recomputed by the UT transform).  FULL folds slots
  * with occ == chunk, FORCE every non-empty slot (DIRECT slots: compression
  * with S0 = 0, mode -> CHUNKWISE).  A range with nothing to fold is a no-op
  * (not an error). */

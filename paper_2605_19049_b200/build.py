@@ -43,14 +43,25 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not needs_build():
         return LIB
     nvcc = os.environ.get("NVCC", "nvcc")
-    cmd = [nvcc, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
-           "-Xcompiler", "-fvisibility=hidden", "-shared", "-o", LIB + ".tmp",
-           f"-I{os.path.join(ROOT, 'include')}", f"-I{NCCL_INC}",
-           "-Xptxas", "-warn-spills", "--expt-relaxed-constexpr",
-           *_sources(), "-ldl", "-lpthread"]
+    flags = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+             "-Xcompiler", "-fvisibility=hidden",
+             f"-I{os.path.join(ROOT, 'include')}", f"-I{NCCL_INC}",
+             "-Xptxas", "-warn-spills", "--expt-relaxed-constexpr"]
     if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-    subprocess.check_call(cmd)
+        flags.append("-Xptxas=-v")
+    # one object per source, compiled in parallel (no relocatable device code:
+    # every kernel is launched from its own translation unit), then one link
+    objdir = os.path.join(PKG, "build")
+    os.makedirs(objdir, exist_ok=True)
+    procs, objs = [], []
+    for src in _sources():
+        obj = os.path.join(objdir, os.path.basename(src) + ".o")
+        objs.append(obj)
+        procs.append((src, subprocess.Popen([nvcc, *flags, "-c", "-o", obj, src])))
+    bad = [src for src, p in procs if p.wait() != 0]
+    if bad:
+        raise subprocess.CalledProcessError(1, f"nvcc {' '.join(bad)}")
+    subprocess.check_call([nvcc, *ARCH, "-shared", "-o", LIB + ".tmp", *objs, "-ldl", "-lpthread"])
     os.replace(LIB + ".tmp", LIB)
     return LIB
 

@@ -499,24 +499,12 @@ static cudaError_t launch_nt(const ChunkArgs &a, cudaStream_t s) {
     return launch_cfg<InT, UT, TPC, WPT, 16, HAS_STATE>(a, s);
 }
 
-static int env_tpc() {
-    static int v = -1;
-    if (v < 0) {
-        const char *e = getenv("LABUF_CHUNK_TPC");   // tuning sweeps only
-        v = e ? atoi(e) : 0;
-    }
-    return v;
-}
-
 template <typename InT, typename UT>
 static cudaError_t launch_t(const ChunkArgs &a, cudaStream_t s) {
+    // (1 or 4 tiles per CTA and 2 warps per tile were measured and rejected,
+    //  DESIGN.md section 6)
     if (a.kind == CK_DIRECT) return launch_nt<InT, UT, kDirectTPC, 1, false>(a, s);
-    switch (env_tpc()) {   // tuning sweeps: 1 = 1 tile x 1 warp, 4 = 4 x 1, 22 = 2 x 2, else 2 tiles x 1 warp
-        case 1: return launch_nt<InT, UT, 1, 1, true>(a, s);
-        case 4: return launch_nt<InT, UT, 4, 1, true>(a, s);
-        case 22: return launch_nt<InT, UT, 2, 2, true>(a, s);
-        default: return launch_nt<InT, UT, kChunkTPC, 1, true>(a, s);
-    }
+    return launch_nt<InT, UT, kChunkTPC, 1, true>(a, s);
 }
 
 cudaError_t launch_chunk(const ChunkArgs &a_in, cudaStream_t s, int64_t *launches) {

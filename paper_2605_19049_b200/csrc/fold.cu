@@ -33,9 +33,11 @@ constexpr int kFoldKCMax = 32;   // tokens per MMA staging chunk (max)
 constexpr int kFoldThreads = 128;
 
 struct FoldSmem {
-    uint32_t S, A, Alo, Bhi, Blo, bar, total;
+    uint32_t S, A, Alo, Bhi, Blo, bar, Ks, Gm, Us, Gs, Bs, total;
 };
-__host__ __device__ inline FoldSmem fold_smem_layout(bool fp32_in, int nj, int kc) {
+// raw_n > 0 (mode ii): room for the n raw keys (fp32), the n x n scaled Gram
+// matrix and the CTA's n x nj delta values recomputed by the UT transform
+__host__ __device__ inline FoldSmem fold_smem_layout(bool fp32_in, int nj, int kc, int raw_n = 0) {
     FoldSmem L;
     uint32_t o = 0;
     L.S = o;   o += (uint32_t)nj * kD * 4;                 // nj state rows
@@ -44,6 +46,11 @@ __host__ __device__ inline FoldSmem fold_smem_layout(bool fp32_in, int nj, int k
     L.Bhi = o; o += (uint32_t)nj * kc * 4;
     L.Blo = o; o += (uint32_t)nj * kc * 4;
     L.bar = o; o += 64;
+    L.Ks = o;  o += (uint32_t)((raw_n + 15) & ~15) * kD * 4;   // rows past raw_n are zero
+    L.Gm = o;  o += (uint32_t)raw_n * raw_n * 4;
+    L.Us = o;  o += (uint32_t)raw_n * nj * 4;
+    L.Gs = o;  o += (uint32_t)raw_n * 4;
+    L.Bs = o;  o += (uint32_t)raw_n * 4;
     L.total = o;
     return L;
 }
@@ -55,8 +62,16 @@ __device__ __forceinline__ uint32_t kmaj_off(int row, int k, int kc) {
     return (uint32_t)((row >> 3) * (kc * 32) + (k >> 2) * 128 + (row & 7) * 16 + (k & 3) * 4);
 }
 
-template <typename InT, typename UT, bool FP32_IN, int kFoldNJ, int KCM>
-__global__ void __launch_bounds__(kFoldThreads, kFoldNJ == 32 && KCM == 16 ? 8 : 4) fold_kernel(const FoldArgs a) {
+// Mode ii (RAW, P:392-399 with reading Z4): the delta values are not read
+// from the buffer but recomputed from the raw records (k_i, v_i, beta_i, G_i)
+// and S0 by the UT transform, per d_v column j of the CTA's tile:
+//   W[i][j] = (S0 k_i)[j]                                     (CUDA cores)
+//   u_i[j]  = beta_i (v_i[j] - e^{G_i} W[i][j]
+//                     - sum_{l<i} e^{G_i-G_l} (k_i.k_l) u_l[j])  (forward substitution)
+// i.e. U = T Diag(beta) (V - Diag(e^G) W) with T = [I + strictLower(Diag(beta)
+// (Gamma (.) K K^T))]^{-1}, then the same tensor-core fold as mode i.
+template <typename InT, typename UT, bool FP32_IN, int kFoldNJ, int KCM, bool RAW>
+__global__ void __launch_bounds__(kFoldThreads, RAW ? 4 : (kFoldNJ == 32 && KCM == 16 ? 8 : 4)) fold_kernel(const FoldArgs a) {
     constexpr int NPAR = kFoldThreads / kFoldNJ;   // token parities per B row
     const int jh = blockIdx.x, h = blockIdx.y, zi = blockIdx.z;
     const int r = a.first + zi;
@@ -67,7 +82,7 @@ __global__ void __launch_bounds__(kFoldThreads, kFoldNJ == 32 && KCM == 16 ? 8 :
     const int KC = a.kc;                           // staging chunk (multiple of 8, <= 32)
 
     extern __shared__ __align__(1024) unsigned char smem[];
-    const FoldSmem L = fold_smem_layout(FP32_IN, kFoldNJ, KC);
+    const FoldSmem L = fold_smem_layout(FP32_IN, kFoldNJ, KC, RAW ? a.kcap : 0);
     float *S_s = reinterpret_cast<float *>(smem + L.S);
     unsigned char *A = smem + L.A, *Alo = smem + L.Alo, *Bhi = smem + L.Bhi, *Blo = smem + L.Blo;
     uint64_t *bar_ld = reinterpret_cast<uint64_t *>(smem + L.bar);
@@ -91,13 +106,23 @@ __global__ void __launch_bounds__(kFoldThreads, kFoldNJ == 32 && KCM == 16 ? 8 :
     float kv[KCM], uv[KCM / NPAR], gv[KCM / NPAR];
     auto load_chunk = [&](int kc0, int kn) {
 #pragma unroll
-        for (int i = 0; i < KCM; ++i)
-            kv[i] = (i < kn) ? to_f(Kb[(size_t)(kc0 + i) * kD + c]) : 0.f;
+        for (int i = 0; i < KCM; ++i) {
+            if constexpr (RAW)
+                kv[i] = (i < kn) ? reinterpret_cast<const float *>(smem + L.Ks)[(kc0 + i) * kD + c] : 0.f;
+            else
+                kv[i] = (i < kn) ? to_f(Kb[(size_t)(kc0 + i) * kD + c]) : 0.f;
+        }
 #pragma unroll
         for (int q = 0; q < KCM / NPAR; ++q) {
             const int i = NPAR * q + ip;
-            uv[q] = (i < kn) ? to_f(Urow[(size_t)(kc0 + i) * kUSub]) : 0.f;
-            gv[q] = (i < kn) ? Gb[kc0 + i] : 0.f;
+            if constexpr (RAW)
+                uv[q] = (i < kn) ? reinterpret_cast<const float *>(smem + L.Us)[(kc0 + i) * kFoldNJ + jb] : 0.f;
+            else
+                uv[q] = (i < kn) ? to_f(Urow[(size_t)(kc0 + i) * kUSub]) : 0.f;
+            if constexpr (RAW)
+                gv[q] = (i < kn) ? reinterpret_cast<const float *>(smem + L.Gs)[kc0 + i] : 0.f;
+            else
+                gv[q] = (i < kn) ? Gb[kc0 + i] : 0.f;
         }
     };
 
@@ -134,7 +159,37 @@ __global__ void __launch_bounds__(kFoldThreads, kFoldNJ == 32 && KCM == 16 ? 8 :
             bulk_g2s(S_s, state_tile, kFoldNJ * kD * 4, bar_ld);
         }
     }
-    load_chunk(0, min(KC, a.kcap));
+    if constexpr (RAW) {
+        // raw records of every token this launch may fold, requested in
+        // batches of 16 loads per thread: keys -> fp32 rows, log decays, betas,
+        // and the thread's raw values v_i[j] (parked in Us)
+        float *Ks = reinterpret_cast<float *>(smem + L.Ks);
+        float *Gs = reinterpret_cast<float *>(smem + L.Gs);
+        float *Bs = reinterpret_cast<float *>(smem + L.Bs);
+        float *Us = reinterpret_cast<float *>(smem + L.Us);
+        const InT *Vb = static_cast<const InT *>(a.p.V) + ((size_t)r * Hv + h) * T * kD;
+        const float *Bb = a.p.B + ((size_t)r * Hv + h) * T;
+        for (int i0 = 0; i0 < a.kcap; i0 += 16) {
+            float t[16];
+#pragma unroll
+            for (int u = 0; u < 16; ++u) t[u] = (i0 + u < a.kcap) ? to_f(Kb[(size_t)(i0 + u) * kD + c]) : 0.f;
+#pragma unroll
+            for (int u = 0; u < 16; ++u) Ks[(i0 + u) * kD + c] = t[u];
+        }
+        for (int i0 = ip; i0 < a.kcap; i0 += 16 * NPAR) {
+            float t[16];
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
+                const int i = i0 + NPAR * u;
+                t[u] = (i < a.kcap) ? to_f(Vb[(size_t)i * kD + jr]) : 0.f;
+            }
+#pragma unroll
+            for (int u = 0; u < 16; ++u) if (i0 + NPAR * u < a.kcap) Us[(i0 + NPAR * u) * kFoldNJ + jb] = t[u];
+        }
+        for (int i = tid; i < a.kcap; i += kFoldThreads) { Gs[i] = Gb[i]; Bs[i] = Bb[i]; }
+    } else {
+        load_chunk(0, min(KC, a.kcap));
+    }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -145,6 +200,107 @@ __global__ void __launch_bounds__(kFoldThreads, kFoldNJ == 32 && KCM == 16 ? 8 :
         if (a.spec) mbar_wait(bar_ld, 0);   // the speculative copy must land before exit
         if (warp == 0) tmem_dealloc<kFoldNJ>(tmem);
         return;
+    }
+    if constexpr (RAW) {
+        const float *Ks = reinterpret_cast<const float *>(smem + L.Ks);
+        const float *Gs = reinterpret_cast<const float *>(smem + L.Gs);
+        const float *Bs = reinterpret_cast<const float *>(smem + L.Bs);
+        float *Gm = reinterpret_cast<float *>(smem + L.Gm);
+        float *Us = reinterpret_cast<float *>(smem + L.Us);
+        const int lane = tid & 31;
+        // (1) scaled strictly-lower Gram matrix  Gm[i][l] = beta_i e^{G_i-G_l} (k_i.k_l), l < i;
+        //     one thread per pair (pairs enumerated row by row), rotated 16-byte
+        //     chunks so the 8 lanes of a shared-memory phase hit distinct bank groups
+        {
+            const int npair = n * (n - 1) / 2;
+            for (int p = tid; p < npair; p += kFoldThreads) {
+                int i = (int)((1.f + sqrtf(1.f + 8.f * (float)p)) * 0.5f);
+                while (i * (i - 1) / 2 > p) --i;
+                while ((i + 1) * i / 2 <= p) ++i;
+                const int l = p - i * (i - 1) / 2;
+                float acc0 = 0.f, acc1 = 0.f;
+#pragma unroll 8
+                for (int cc = 0; cc < kD / 4; cc += 2) {
+                    const int c0 = (cc + lane) & (kD / 4 - 1), c1 = (cc + 1 + lane) & (kD / 4 - 1);
+                    const float4 x0 = *reinterpret_cast<const float4 *>(Ks + i * kD + 4 * c0);
+                    const float4 y0 = *reinterpret_cast<const float4 *>(Ks + l * kD + 4 * c0);
+                    const float4 x1 = *reinterpret_cast<const float4 *>(Ks + i * kD + 4 * c1);
+                    const float4 y1 = *reinterpret_cast<const float4 *>(Ks + l * kD + 4 * c1);
+                    acc0 = fmaf(x0.x, y0.x, fmaf(x0.y, y0.y, fmaf(x0.z, y0.z, fmaf(x0.w, y0.w, acc0))));
+                    acc1 = fmaf(x1.x, y1.x, fmaf(x1.y, y1.y, fmaf(x1.z, y1.z, fmaf(x1.w, y1.w, acc1))));
+                }
+                Gm[i * n + l] = Bs[i] * expf(Gs[i] - Gs[l]) * (acc0 + acc1);
+            }
+        }
+        // (2) right-hand side  Us[i][j] = beta_i (v_i[j] - e^{G_i} (S0 k_i)[j]); thread (jb, ip),
+        //     4 tokens per pass so each state chunk read serves 4 dot products;
+        //     rotated 16-byte chunks: the lanes (rows jb) hit distinct bank groups
+        if (!zero_s0) mbar_wait(bar_ld, 0);
+        for (int i0 = ip; i0 < n; i0 += 4 * NPAR) {
+            // tokens i0 + NPAR u (u < 4): key rows at a constant 4 x 512 B stride
+            // (rows past kcap are zero), so one rotated chunk offset addresses all five loads
+            float w[4] = {0.f, 0.f, 0.f, 0.f};
+            if (!zero_s0) {
+                const char *srow = reinterpret_cast<const char *>(S_s + jb * kD);
+                const char *krow = reinterpret_cast<const char *>(Ks + i0 * kD);
+#pragma unroll 8
+                for (int cc = 0; cc < kD / 4; ++cc) {
+                    const int off = ((cc + jb) & (kD / 4 - 1)) * 16;
+                    const float4 sv = *reinterpret_cast<const float4 *>(srow + off);
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const float4 kv4 = *reinterpret_cast<const float4 *>(krow + off + u * NPAR * kD * 4);
+                        w[u] = fmaf(sv.x, kv4.x, w[u]);
+                        w[u] = fmaf(sv.y, kv4.y, w[u]);
+                        w[u] = fmaf(sv.z, kv4.z, w[u]);
+                        w[u] = fmaf(sv.w, kv4.w, w[u]);
+                    }
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int i = i0 + NPAR * u;
+                if (i < n) Us[i * kFoldNJ + jb] = Bs[i] * (Us[i * kFoldNJ + jb] - expf(Gs[i]) * w[u]);
+            }
+        }
+        __syncthreads();
+        // (3) forward substitution down each column (lane = d_v row of the tile);
+        //     up to 32 tokens the column lives in registers and each row's sum
+        //     runs on two accumulator chains (Gm reads are warp broadcasts)
+        if (warp == 0) {
+            if (n <= 32) {
+                float u[32];
+#pragma unroll
+                for (int i = 0; i < 32; ++i) u[i] = i < n ? Us[i * kFoldNJ + lane] : 0.f;
+#pragma unroll
+                for (int i = 1; i < 32; ++i) {
+                    if (i < n) {
+                        float x0 = u[i], x1 = 0.f;
+#pragma unroll
+                        for (int l = 0; l < i; l += 2) {
+                            x0 = fmaf(-Gm[i * n + l], u[l], x0);
+                            if (l + 1 < i) x1 = fmaf(-Gm[i * n + l + 1], u[l + 1], x1);
+                        }
+                        u[i] = x0 + x1;
+                    }
+                }
+#pragma unroll
+                for (int i = 0; i < 32; ++i) if (i < n) Us[i * kFoldNJ + lane] = u[i];
+            } else {
+                for (int i = 1; i < n; ++i) {
+                    float x0 = Us[i * kFoldNJ + lane], x1 = 0.f;
+                    int l = 0;
+                    for (; l + 1 < i; l += 2) {
+                        x0 = fmaf(-Gm[i * n + l], Us[l * kFoldNJ + lane], x0);
+                        x1 = fmaf(-Gm[i * n + l + 1], Us[(l + 1) * kFoldNJ + lane], x1);
+                    }
+                    if (l < i) x0 = fmaf(-Gm[i * n + l], Us[l * kFoldNJ + lane], x0);
+                    Us[i * kFoldNJ + lane] = x0 + x1;
+                }
+            }
+        }
+        __syncthreads();
+        load_chunk(0, min(KC, n));
     }
     const float g_last = Gb[n - 1];
     const uint32_t idesc = idesc_tf32(128, kFoldNJ);
@@ -244,10 +400,10 @@ __global__ void __launch_bounds__(kFoldThreads, kFoldNJ == 32 && KCM == 16 ? 8 :
     }
 }
 
-template <typename InT, typename UT, bool FP32_IN, int NJ, int KCM>
+template <typename InT, typename UT, bool FP32_IN, int NJ, int KCM, bool RAW>
 static cudaError_t launch_fold_cfg(const FoldArgs &a, cudaStream_t s) {
-    const FoldSmem L = fold_smem_layout(FP32_IN, NJ, a.kc);
-    auto kfn = fold_kernel<InT, UT, FP32_IN, NJ, KCM>;
+    const FoldSmem L = fold_smem_layout(FP32_IN, NJ, a.kc, RAW ? a.kcap : 0);
+    auto kfn = fold_kernel<InT, UT, FP32_IN, NJ, KCM, RAW>;
     cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
     if (e != cudaSuccess) return e;
     dim3 grid(kD / NJ, a.dm.Hv, a.n);
@@ -259,11 +415,14 @@ template <typename InT, typename UT, bool FP32_IN>
 static cudaError_t launch_fold_t(const FoldArgs &a, cudaStream_t s) {
     // LABUF_FOLD_NJ: d_v rows per CTA (32 or 64; tuning sweeps)
     static const int nj = getenv("LABUF_FOLD_NJ") ? atoi(getenv("LABUF_FOLD_NJ")) : 32;
+    if (a.raw)
+        return a.kc <= 16 ? launch_fold_cfg<InT, UT, FP32_IN, 32, 16, true>(a, s)
+                          : launch_fold_cfg<InT, UT, FP32_IN, 32, 32, true>(a, s);
     if (nj == 64)
-        return a.kc <= 16 ? launch_fold_cfg<InT, UT, FP32_IN, 64, 16>(a, s)
-                          : launch_fold_cfg<InT, UT, FP32_IN, 64, 32>(a, s);
-    return a.kc <= 16 ? launch_fold_cfg<InT, UT, FP32_IN, 32, 16>(a, s)
-                      : launch_fold_cfg<InT, UT, FP32_IN, 32, 32>(a, s);
+        return a.kc <= 16 ? launch_fold_cfg<InT, UT, FP32_IN, 64, 16, false>(a, s)
+                          : launch_fold_cfg<InT, UT, FP32_IN, 64, 32, false>(a, s);
+    return a.kc <= 16 ? launch_fold_cfg<InT, UT, FP32_IN, 32, 16, false>(a, s)
+                      : launch_fold_cfg<InT, UT, FP32_IN, 32, 32, false>(a, s);
 }
 
 cudaError_t launch_fold(const FoldArgs &a_in, cudaStream_t s, int64_t *launches) {

@@ -72,6 +72,7 @@ struct FoldArgs {
     int kcap;           // host bound on the records any slot of the launch folds
     int spec;           // host mirror: every slot of the range folds (issue the state copy at entry)
     int kc;             // staging chunk (set by launch_fold)
+    int raw = 0;        // mode ii: recompute u from the raw records (keep_raw) by the UT transform
 };
 
 struct RecArgs {

@@ -268,7 +268,10 @@ la_status la_decode_step(la_buf *b, int32_t first, int32_t n, const void *q, con
 la_status la_flush(la_buf *b, int32_t first, int32_t n, int32_t kind, la_stream stream) {
     la_status st;
     if ((st = check_handle(b)) != LA_OK || (st = check_range(b, first, n)) != LA_OK) return st;
+    const bool raw = (kind & LA_FLUSH_RAW) != 0;
+    kind &= ~LA_FLUSH_RAW;
     if (kind != LA_FLUSH_FULL && kind != LA_FLUSH_FORCE) return fail(LA_ERR_INVALID, "bad flush kind");
+    if (raw && !b->cfg.keep_raw) return fail(LA_ERR_INVALID, "LA_FLUSH_RAW needs a handle created with keep_raw = 1");
     bool any = false, all = true;
     int kcap = 0;
     for (int r = first; r < first + n; ++r) {
@@ -287,6 +290,7 @@ la_status la_flush(la_buf *b, int32_t first, int32_t n, int32_t kind, la_stream 
     FoldArgs a;
     a.dm = b->dm; a.p = b->p; a.first = first; a.n = n;
     a.kind = kind == LA_FLUSH_FULL ? FK_FULL : FK_FORCE; a.nacc = nullptr; a.n_draft = 0; a.kcap = kcap; a.spec = all;
+    a.raw = raw ? 1 : 0;
     cudaError_t e = launch_fold(a, static_cast<cudaStream_t>(stream), &b->launches);
     if (e != cudaSuccess) return cuda_fail(e, "flush launch");
     for (int r = first; r < first + n; ++r) {

@@ -20,7 +20,7 @@ LIB_PATH = os.environ.get("LABUF_LIB", os.path.join(_PKG, "liblabuf.so"))
 LA_OK, LA_ERR_INVALID, LA_ERR_UNSUPPORTED, LA_ERR_CAPACITY, LA_ERR_MODE, LA_ERR_CUDA, LA_ERR_NCCL = range(7)
 LA_DT_F32, LA_DT_BF16, LA_DT_F16 = 0, 1, 2
 LA_MODE_CHUNKWISE, LA_MODE_DIRECT = 0, 1
-LA_FLUSH_FULL, LA_FLUSH_FORCE = 0, 1
+LA_FLUSH_FULL, LA_FLUSH_FORCE, LA_FLUSH_RAW = 0, 1, 2   # RAW is a flag OR-ed into FULL/FORCE (mode ii)
 STATUS_BITS = {"bad_alpha": 0x1, "bad_beta": 0x2, "nonfinite": 0x4, "bad_nacc": 0x8}
 
 _STATUS_NAMES = {0: "LA_OK", 1: "LA_ERR_INVALID", 2: "LA_ERR_UNSUPPORTED", 3: "LA_ERR_CAPACITY",

@@ -1,0 +1,148 @@
+"""Config 5 driver: a stack of GDN layers serving a mixed batch (SURVEY §8d
+config 5, BASELINE.json configs[4]).
+
+Per layer two handles of the C ABI: a CHUNKWISE handle for the long-context
+requests (buffered decode + flush, u fp32) and a DIRECT handle for the short
+ones (KV-only decode, u fp16, no state is ever created for them, P:35,
+P:200-213).  Every slot of a handle sits in one contiguous range, so one call
+per handle per layer serves the whole batch.  Host logic only: argument
+marshalling and call ordering; every arithmetic step runs in the library's
+kernels.
+
+Ragged starting points use contiguous groups so each call still covers one
+range: long slots are staggered over occupancies 0..C-1 (group g holds occ =
+g, so flushes spread over the C steps of a cycle), short slots start at
+group-wise context lengths L0 (a KV-only prefill per group).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import torch
+
+from . import labuf as L
+
+
+@dataclass
+class StackSpec:
+    n_layers: int = 36
+    n_long: int = 1536
+    n_short: int = 512
+    n_qk_heads: int = 16
+    n_v_heads: int = 32
+    chunk: int = 16
+    short_cap: int = 128
+    short_l0: tuple = (16, 40, 64, 96)     # context length per short group (U{16..96} in 4 groups)
+    in_dtype: str = "bf16"
+
+
+def long_groups(spec: StackSpec):
+    """[(first, n, occupancy)] of the staggered long slots (n_long split into C groups)."""
+    C, n = spec.chunk, spec.n_long
+    base, extra = divmod(n, C)
+    out, first = [], 0
+    for g in range(C):
+        m = base + (1 if g < extra else 0)
+        out.append((first, m, g))
+        first += m
+    return out
+
+
+def short_groups(spec: StackSpec):
+    """[(first, n, L0)] of the short slots."""
+    G, n = len(spec.short_l0), spec.n_short
+    base, extra = divmod(n, G)
+    out, first = [], 0
+    for g, l0 in enumerate(spec.short_l0):
+        m = base + (1 if g < extra else 0)
+        out.append((first, m, l0))
+        first += m
+    return out
+
+
+@dataclass
+class Layer:
+    long: L.LaBuf
+    short: L.LaBuf | None
+
+
+@dataclass
+class GdnStack:
+    spec: StackSpec
+    device: torch.device
+    layers: list = field(default_factory=list)
+
+    @classmethod
+    def create(cls, spec: StackSpec, device):
+        st = cls(spec, torch.device(device))
+        for _ in range(spec.n_layers):
+            lc = L.make_config(spec.n_long, spec.n_qk_heads, spec.n_v_heads, chunk=spec.chunk,
+                               in_dtype=spec.in_dtype, u_dtype="f32", validate=False)
+            sb = None
+            if spec.n_short:
+                sc = L.make_config(spec.n_short, spec.n_qk_heads, spec.n_v_heads, chunk=spec.chunk,
+                                   short_cap=spec.short_cap, in_dtype=spec.in_dtype,
+                                   u_dtype="f16" if spec.in_dtype == "bf16" else "f32", validate=False)
+                sb = L.LaBuf(sc, device=st.device)
+            st.layers.append(Layer(L.LaBuf(lc, device=st.device), sb))
+        return st
+
+    def reset(self, states):
+        """states[l]: fp32 [n_long, Hv, d, d] start states of layer l's long slots."""
+        for lay, S0 in zip(self.layers, states):
+            lay.long.reset(zero_state=False)
+            lay.long.state.copy_(S0)
+            if lay.short is not None:
+                lay.short.reset(mode=L.LA_MODE_DIRECT, zero_state=False)
+
+    def warmup(self, long_tok, short_tok):
+        """Bring the slots to their ragged starting points.
+
+        long_tok(l, t)  -> decode inputs of token t for ALL long slots of layer l
+                           (dict q,k,v,alpha,beta [n_long, ...], token axis squeezed)
+        short_tok(l, g) -> prefill inputs of short group g ([n_g, L0_g, ...])
+        Outputs of the warm-up are written to scratch and returned per call
+        for tests: {("long", l, t): o, ("short", l, g): o}."""
+        outs = {}
+        spec = self.spec
+        Hv, d = spec.n_v_heads, 128
+        for l, lay in enumerate(self.layers):
+            groups = long_groups(spec)
+            for t in range(spec.chunk - 1):
+                # groups with occupancy > t decode token t (a suffix of the range)
+                first = next((f for f, m, occ in groups if occ > t), None)
+                if first is None:
+                    break
+                x = long_tok(l, t)
+                n = spec.n_long - first
+                o = torch.empty(n, Hv, d, dtype=torch.float32, device=self.device)
+                lay.long.decode_step(first, *(x[k][first:] for k in ("q", "k", "v", "alpha", "beta")), o)
+                outs[("long", l, t)] = (first, o)
+            if lay.short is not None:
+                for g, (first, m, l0) in enumerate(short_groups(spec)):
+                    x = short_tok(l, g)
+                    o = torch.empty(m, l0, Hv, d, dtype=torch.float32, device=self.device)
+                    lay.short.direct_short(first, x["q"], x["k"], x["v"], x["alpha"], x["beta"], o)
+                    outs[("short", l, g)] = (first, o)
+        return outs
+
+    def step(self, long_in, short_in, long_out, short_out):
+        """One decode step of the whole stack: per layer, one buffered decode
+        call over all long slots (+ the FULL flush of the slots it filled) and
+        one KV-only call over all short slots.  *_in[l] / *_out[l] are the
+        layer's device tensors (short ones with a token axis of 1)."""
+        for l, lay in enumerate(self.layers):
+            x = long_in[l]
+            lay.long.decode_step(0, x["q"], x["k"], x["v"], x["alpha"], x["beta"], long_out[l])
+            lay.long.flush(0, self.spec.n_long, L.LA_FLUSH_FULL)
+            if lay.short is not None:
+                y = short_in[l]
+                lay.short.direct_short(0, y["q"], y["k"], y["v"], y["alpha"], y["beta"], short_out[l])
+
+    def footprint_bytes(self):
+        tot = 0
+        for lay in self.layers:
+            for b in (lay.long, lay.short):
+                if b is not None:
+                    tot += b.sizes.state_bytes + b.sizes.buffer_bytes + b.sizes.meta_bytes
+        return tot
