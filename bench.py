@@ -51,6 +51,7 @@ def parse_args():
     p.add_argument("--u-dtype", default="f32", choices=["f32", "f16"])
     p.add_argument("--no-rows", action="store_true", help="skip the verify / direct rows")
     p.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    p.add_argument("--no-overlap", action="store_true", help="launch without PDL (la_set_overlap 0)")
     p.add_argument("--seed", type=int, default=1002)
     return p.parse_args()
 
@@ -311,6 +312,9 @@ def main():
     for b in bufs:
         b.reset(zero_state=False)
     fill_states(torch, bufs, seed0)
+    torch.cuda.synchronize()
+    for b in bufs:
+        b.set_overlap(not args.no_overlap)   # PDL for the buffered AND the recurrent kernels
     inputs = [make_inputs(torch, B, Hk, Hv, NL, args.in_dtype, seed0 + 10 * (t + 1), dev) for t in range(C)]
     stream = torch.cuda.Stream(device=dev)
     torch.cuda.synchronize()
@@ -383,7 +387,7 @@ def main():
                    "state": "fp32", "parallelism": f"dp{world} (requests partitioned, no collective)",
                    "step": f"one buffer cycle: {C} decode steps + 1 flush, x {NL} layer instances",
                    "l2": f"inputs larger than L2: {NL} layers x {B * lb.st / 2**20:.0f} MiB state rotated per step",
-                   "cuda_graphs": True},
+                   "cuda_graphs": True, "launch_overlap": not args.no_overlap},
         "us_per_token": us_per_token,
         "tokens_per_s_per_gpu": B / (us_per_token * 1e-6),
         "hbm_frac_of_8TBs": step_bytes / (ms_per_step * 1e-3) / 8e12,
@@ -513,6 +517,9 @@ def extra_rows(torch, L, cost, dev, stream, seed, K, W, peak, args):
     for b in bufs:
         b.reset(zero_state=False)
     fill_states(torch, bufs, seed + 1)
+    torch.cuda.synchronize()
+    for b in bufs:
+        b.set_overlap(not args.no_overlap)
     xs2 = [make_inputs(torch, B2, Hk, Hv, NL2, args.in_dtype, seed + 2 + t, dev) for t in range(C2)]
 
     def dec2():
@@ -554,6 +561,9 @@ def extra_rows(torch, L, cost, dev, stream, seed, K, W, peak, args):
     for b in bufs:
         b.reset(zero_state=False)
     fill_states(torch, bufs, seed)
+    torch.cuda.synchronize()
+    for b in bufs:
+        b.set_overlap(not args.no_overlap)
     nacc = [sd.n_accepted(seed + 10 + l, B3, N3, device=dev) for l in range(NL3)]
     xs = []
     for l in range(NL3):
@@ -612,6 +622,7 @@ def extra_rows(torch, L, cost, dev, stream, seed, K, W, peak, args):
     B4, L0, NS = 1024, 64, 32
     cfg = L.make_config(B4, Hk, Hv, chunk=16, short_cap=128, u_dtype="f16")
     b4 = L.LaBuf(cfg, device=dev)
+    b4.set_overlap(not args.no_overlap)
     lb4 = cost.LayerBytes.make(Hk, Hv, D, 2, 2)
     pre = sd.tokens(seed + 30, B4, L0, Hk, Hv, D, device=dev)
     pre["o"] = torch.empty(B4, L0, Hv, D, dtype=torch.float32, device=dev)
@@ -640,6 +651,7 @@ def extra_rows(torch, L, cost, dev, stream, seed, K, W, peak, args):
     # recurrent baseline at the same batch and the same tokens
     cfgr = L.make_config(B4, Hk, Hv, chunk=16)
     br = L.LaBuf(cfgr, device=dev)
+    br.set_overlap(not args.no_overlap)
     br.reset(zero_state=True)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     sq = [{k: v[:, 0].contiguous() for k, v in x.items()} for x in steps]

@@ -225,6 +225,21 @@ LA_API la_status la_recurrent_commit(la_buf *buf, int32_t first, int32_t n, int3
 
 /* Canonical state export/import of one slot: fp32 [Hv][d_v][d_k], device
  * pointers, async on `stream`. */
+/* Launch overlap (programmatic dependent launch, B200 griddepcontrol): with
+ * enable = 1 every kernel of this handle is launched as a programmatic
+ * dependent of the previous kernel on the stream, so its CTAs start while
+ * that kernel drains; when the previous kernel cannot have written this
+ * handle's state (the library tracks its own launches: a fold, reset,
+ * recurrent step/commit or la_state_set of the same handle on the same
+ * stream disables it), the state tiles are requested before
+ * griddepcontrol.wait and stream in during that drain.  Inputs, counters,
+ * records and outputs are always accessed after the wait.
+ * Contract when enabled: a kernel that is NOT a la_* call and writes this
+ * handle's state must not be the kernel enqueued immediately before a la_*
+ * call of the handle on the same stream (put an event/sync or any la_* call
+ * in between).  Default 0 (off).  LA_ERR_INVALID on enable not 0/1. */
+LA_API la_status la_set_overlap(la_buf *buf, int32_t enable);
+
 LA_API la_status la_state_get(la_buf *buf, int32_t slot, float *dst, la_stream stream);
 LA_API la_status la_state_set(la_buf *buf, int32_t slot, const float *src, la_stream stream);
 

@@ -212,7 +212,16 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
         mbar_init(full, 1);
         mbar_init(recs, 1);
         fence_mbar_init();
+        if (HAS_STATE && a.pdl_early) {
+            // the state tile is not written by the grid this one overlaps
+            // (launch overlap), so it streams in while that grid drains
+            mbar_arrive_expect_tx(full, fixed_bytes);
+            bulk_g2s(smem + L.S, a.p.state + (((size_t)r * Hv + h) * kD + (size_t)tile0 * 32) * kD,
+                     TPC * 32 * kD * 4, full);
+        }
     }
+    if (a.pdl) pdl_wait();   // inputs, counters and records may come from the previous grid
+    pdl_trigger();
     // alpha / beta of the new tokens (lane t), in flight with the copies
     float al_l = 1.f, be_l = 0.f;
     if (lane < n_new) {
@@ -222,10 +231,12 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
     __syncthreads();
     int ticket = 0;
     if (tid == 0) {
-        mbar_arrive_expect_tx(full, fixed_bytes);
-        if (HAS_STATE)
-            bulk_g2s(smem + L.S, a.p.state + (((size_t)r * Hv + h) * kD + (size_t)tile0 * 32) * kD,
-                     TPC * 32 * kD * 4, full);
+        if (!(HAS_STATE && a.pdl_early)) {
+            mbar_arrive_expect_tx(full, fixed_bytes);
+            if (HAS_STATE)
+                bulk_g2s(smem + L.S, a.p.state + (((size_t)r * Hv + h) * kD + (size_t)tile0 * 32) * kD,
+                         TPC * 32 * kD * 4, full);
+        }
         const int j0v = (direct ? a.p.len : a.p.occ)[r] + a.j_add;
         const int jbv = (j0v + 3) & ~3;
         *j0_s = j0v;
@@ -486,8 +497,7 @@ static cudaError_t launch_cfg(const ChunkArgs &a, cudaStream_t s) {
     auto kfn = chunk_cta_kernel<InT, UT, TPC, WPT, NT, HAS_STATE, MINB < 1 ? 1 : MINB>;
     cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.bytes);
     if (e != cudaSuccess) return e;
-    kfn<<<dim3(4 / TPC, a.dm.Hv, a.n), TPC * WPT * 32, L.bytes, s>>>(a);
-    return cudaGetLastError();
+    return launch_k(kfn, dim3(4 / TPC, a.dm.Hv, a.n), dim3(TPC * WPT * 32), L.bytes, s, a.pdl != 0, a);
 }
 
 template <typename InT, typename UT, int TPC, int WPT, bool HAS_STATE>

@@ -122,6 +122,34 @@ __device__ __forceinline__ void bulk_s2g(void *dst_gmem, const void *src_smem, u
     asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
                  ::"l"(dst_gmem), "r"(smem_u32(src_smem)), "r"(bytes) : "memory");
 }
+// Programmatic dependent launch (PDL): wait for the preceding grid's memory
+// to be visible / let the next PDL-launched grid start its CTAs.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+// Host: launch kfn<<<g, b, smem, s>>>(arg), as a programmatic dependent of
+// the previous kernel on the stream when pdl (its CTAs may start while that
+// kernel drains; everything the kernel reads that another grid may write
+// must come after pdl_wait()).
+template <typename Kern, typename Arg>
+inline cudaError_t launch_k(Kern kfn, dim3 g, dim3 b, size_t smem, cudaStream_t s, bool pdl, const Arg &arg) {
+    if (!pdl) {
+        kfn<<<g, b, smem, s>>>(arg);
+        return cudaGetLastError();
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = g;
+    cfg.blockDim = b;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kfn, arg);
+}
+
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read0() {
     asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");

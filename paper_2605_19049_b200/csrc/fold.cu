@@ -135,8 +135,13 @@ __global__ void __launch_bounds__(kFoldThreads, RAW ? 4 : (kFoldNJ == 32 && KCM 
         fence_mbar_init();
         if (a.spec) {
             mbar_arrive_expect_tx(bar_ld, kFoldNJ * kD * 4);
-            bulk_g2s(S_s, state_tile, kFoldNJ * kD * 4, bar_ld);
+            if (a.pdl_early) bulk_g2s(S_s, state_tile, kFoldNJ * kD * 4, bar_ld);
         }
+    }
+    if (a.pdl) pdl_wait();   // counters, records (and the state unless pdl_early) may come from the previous grid
+    pdl_trigger();
+    if (tid == 32) {
+        if (a.spec && !a.pdl_early) bulk_g2s(S_s, state_tile, kFoldNJ * kD * 4, bar_ld);
         const int mode = a.p.mode[r], occ = a.p.occ[r], len = a.p.len[r];
         int n = 0;
         bool zero_s0 = false;
@@ -406,9 +411,7 @@ static cudaError_t launch_fold_cfg(const FoldArgs &a, cudaStream_t s) {
     auto kfn = fold_kernel<InT, UT, FP32_IN, NJ, KCM, RAW>;
     cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
     if (e != cudaSuccess) return e;
-    dim3 grid(kD / NJ, a.dm.Hv, a.n);
-    kfn<<<grid, kFoldThreads, L.total, s>>>(a);
-    return cudaGetLastError();
+    return launch_k(kfn, dim3(kD / NJ, a.dm.Hv, a.n), dim3(kFoldThreads), L.total, s, a.pdl != 0, a);
 }
 
 template <typename InT, typename UT, bool FP32_IN>

@@ -21,6 +21,13 @@ struct Dims {
     int in_dt, u_dt, keep_raw, validate;
 };
 
+// Launch overlap (la_set_overlap, programmatic dependent launch): pdl = the
+// kernel is launched as a programmatic dependent of the previous kernel on
+// the stream and reads nothing another grid may write before
+// griddepcontrol.wait; pdl_early = the previous kernel cannot have written
+// this handle's state, so the state tiles are requested BEFORE the wait and
+// stream in while that kernel drains.  Every kernel triggers its dependents
+// (griddepcontrol.launch_dependents) once all its CTAs are running.
 struct Ptrs {
     float *state;            // [R][Hv][d][d]
     void *K;                 // [R][Hk][T][d] in_dt
@@ -54,6 +61,7 @@ struct ChunkArgs {
     const float *alpha, *beta;
     float *o;           // may be null (prefill without outputs)
     int dbg;            // tuning experiments only (LABUF_DEBUG): 1 = skip compute, 2 = skip record copies
+    int pdl = 0, pdl_early = 0;   // see Ptrs/launch overlap below
 };
 
 enum FoldKind : int {
@@ -73,6 +81,7 @@ struct FoldArgs {
     int spec;           // host mirror: every slot of the range folds (issue the state copy at entry)
     int kc;             // staging chunk (set by launch_fold)
     int raw = 0;        // mode ii: recompute u from the raw records (keep_raw) by the UT transform
+    int pdl = 0, pdl_early = 0;
 };
 
 struct RecArgs {
@@ -85,6 +94,7 @@ struct RecArgs {
     float *o;
     float *temp;        // recurrent verify: [n][n_draft][Hv][d][d]
     const int *nacc;    // recurrent commit
+    int pdl = 0, pdl_early = 0;
 };
 
 // Launchers: return cudaSuccess or the launch error; *launches += kernels.

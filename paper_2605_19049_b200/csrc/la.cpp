@@ -54,9 +54,32 @@ struct la_buf {
     int device;
     std::vector<int32_t> occ, len, mode, pending;   // host mirror
     int64_t launches = 0;
+    int overlap = 0;                                 // la_set_overlap
 };
 
 namespace {
+
+// The library's last kernel launch on this host thread: whose state it was,
+// on which stream, and whether it wrote that state.  A launch with overlap
+// requests its state tiles before griddepcontrol.wait only if the kernel it
+// overlaps (the previous one on the stream) cannot have written them.
+struct LastLaunch {
+    const void *state = nullptr;
+    cudaStream_t s = nullptr;
+    bool wrote = false;
+};
+thread_local LastLaunch g_last;
+
+template <class Args>
+void overlap_flags(const la_buf *b, cudaStream_t s, Args &a) {
+    a.pdl = b->overlap;
+    a.pdl_early = b->overlap && !(g_last.s == s && g_last.wrote && g_last.state == b->p.state);
+}
+void note_launch(const la_buf *b, cudaStream_t s, bool wrote_state) {
+    g_last.state = b->p.state;
+    g_last.s = s;
+    g_last.wrote = wrote_state;
+}
 
 la_status check_config(const la_config *c) {
     if (!c) return fail(LA_ERR_INVALID, "null config");
@@ -161,8 +184,10 @@ cudaError_t run_chunk(la_buf *b, int first, int n, int n_tok, int j0_cap, int to
             a.alpha = alpha + sq * b->dm.Hv;
             a.beta = beta + sq * b->dm.Hv;
             a.o = o ? o + sq * b->dm.Hv * d : nullptr;
+            overlap_flags(b, s, a);
             cudaError_t e = launch_chunk(a, s, &b->launches);
             if (e != cudaSuccess) return e;
+            note_launch(b, s, false);
         }
     }
     return cudaSuccess;
@@ -232,6 +257,7 @@ la_status la_request_reset(la_buf *b, int32_t first, int32_t n, int32_t mode, in
     cudaError_t e = launch_reset(b->dm, b->p, first, n, mode, zero_state ? 1 : 0,
                                  static_cast<cudaStream_t>(stream), &b->launches);
     if (e != cudaSuccess) return cuda_fail(e, "reset launch");
+    note_launch(b, static_cast<cudaStream_t>(stream), zero_state != 0);
     // status word: cleared by a reset covering slot 0
     if (first == 0) {
         e = cudaMemsetAsync(b->p.status, 0, sizeof(unsigned), static_cast<cudaStream_t>(stream));
@@ -291,8 +317,10 @@ la_status la_flush(la_buf *b, int32_t first, int32_t n, int32_t kind, la_stream 
     a.dm = b->dm; a.p = b->p; a.first = first; a.n = n;
     a.kind = kind == LA_FLUSH_FULL ? FK_FULL : FK_FORCE; a.nacc = nullptr; a.n_draft = 0; a.kcap = kcap; a.spec = all;
     a.raw = raw ? 1 : 0;
+    overlap_flags(b, static_cast<cudaStream_t>(stream), a);
     cudaError_t e = launch_fold(a, static_cast<cudaStream_t>(stream), &b->launches);
     if (e != cudaSuccess) return cuda_fail(e, "flush launch");
+    note_launch(b, static_cast<cudaStream_t>(stream), true);
     for (int r = first; r < first + n; ++r) {
         if (kind == LA_FLUSH_FULL) {
             if (b->mode[r] == LA_MODE_CHUNKWISE && b->occ[r] == b->cfg.chunk) b->occ[r] = 0;
@@ -345,8 +373,10 @@ la_status la_commit_accepted(la_buf *b, int32_t first, int32_t n, const int32_t 
     int occ_max = 0;
     for (int r = first; r < first + n; ++r) occ_max = std::max(occ_max, b->occ[r]);
     a.kind = FK_COMMIT; a.nacc = n_accepted; a.n_draft = nd; a.kcap = occ_max + nd; a.spec = 0;
+    overlap_flags(b, static_cast<cudaStream_t>(stream), a);
     cudaError_t e = launch_fold(a, static_cast<cudaStream_t>(stream), &b->launches);
     if (e != cudaSuccess) return cuda_fail(e, "commit launch");
+    note_launch(b, static_cast<cudaStream_t>(stream), true);
     for (int r = first; r < first + n; ++r) { b->occ[r] = 0; b->pending[r] = 0; }
     return LA_OK;
 }
@@ -395,8 +425,10 @@ la_status la_prefill(la_buf *b, int32_t first, int32_t n, int32_t n_tok, const v
         FoldArgs f;
         f.dm = b->dm; f.p = b->p; f.first = first; f.n = n; f.kind = FK_FORCE; f.nacc = nullptr; f.n_draft = 0;
         f.kcap = cn; f.spec = 1;
+        overlap_flags(b, s, f);
         e = launch_fold(f, s, &b->launches);
         if (e != cudaSuccess) return cuda_fail(e, "prefill fold launch");
+        note_launch(b, s, true);
     }
     return LA_OK;
 }
@@ -415,8 +447,10 @@ la_status la_recurrent_step(la_buf *b, int32_t first, int32_t n, const void *q, 
     RecArgs a{};
     a.dm = b->dm; a.p = b->p; a.first = first; a.n = n; a.n_draft = 1;
     a.q = q; a.k = k; a.v = v; a.alpha = alpha; a.beta = beta; a.o = o;
+    overlap_flags(b, static_cast<cudaStream_t>(stream), a);
     cudaError_t e = launch_recurrent_step(a, static_cast<cudaStream_t>(stream), &b->launches);
     if (e != cudaSuccess) return cuda_fail(e, "recurrent step launch");
+    note_launch(b, static_cast<cudaStream_t>(stream), true);
     return LA_OK;
 }
 
@@ -436,8 +470,10 @@ la_status la_recurrent_verify(la_buf *b, int32_t first, int32_t n, int32_t n_dra
     RecArgs a{};
     a.dm = b->dm; a.p = b->p; a.first = first; a.n = n; a.n_draft = n_draft;
     a.q = q; a.k = k; a.v = v; a.alpha = alpha; a.beta = beta; a.o = o; a.temp = temp;
+    overlap_flags(b, static_cast<cudaStream_t>(stream), a);
     cudaError_t e = launch_recurrent_verify(a, static_cast<cudaStream_t>(stream), &b->launches);
     if (e != cudaSuccess) return cuda_fail(e, "recurrent verify launch");
+    note_launch(b, static_cast<cudaStream_t>(stream), false);
     return LA_OK;
 }
 
@@ -452,8 +488,18 @@ la_status la_recurrent_commit(la_buf *b, int32_t first, int32_t n, int32_t n_dra
     RecArgs a{};
     a.dm = b->dm; a.p = b->p; a.first = first; a.n = n; a.n_draft = n_draft;
     a.nacc = n_accepted; a.temp = const_cast<float *>(temp);
+    overlap_flags(b, static_cast<cudaStream_t>(stream), a);
     cudaError_t e = launch_recurrent_commit(a, static_cast<cudaStream_t>(stream), &b->launches);
     if (e != cudaSuccess) return cuda_fail(e, "recurrent commit launch");
+    note_launch(b, static_cast<cudaStream_t>(stream), true);
+    return LA_OK;
+}
+
+la_status la_set_overlap(la_buf *b, int32_t enable) {
+    la_status st;
+    if ((st = check_handle(b)) != LA_OK) return st;
+    if (enable != 0 && enable != 1) return fail(LA_ERR_INVALID, "enable must be 0 or 1");
+    b->overlap = enable;
     return LA_OK;
 }
 
@@ -478,6 +524,7 @@ la_status la_state_set(la_buf *b, int32_t slot, const float *src, la_stream stre
     cudaError_t e = cudaMemcpyAsync(b->p.state + (size_t)slot * b->dm.Hv * kD * kD, src, bytes,
                                     cudaMemcpyDeviceToDevice, static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(e, "state_set copy");
+    note_launch(b, static_cast<cudaStream_t>(stream), true);
     return LA_OK;
 }
 

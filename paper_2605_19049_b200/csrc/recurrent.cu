@@ -41,6 +41,13 @@ __global__ void __launch_bounds__(256) recurrent_step_kernel(const RecArgs a) {
         mbar_init(bar, 1);
         fence_mbar_init();
         mbar_arrive_expect_tx(bar, GR * kD * 4);
+        if (a.pdl_early)
+#pragma unroll
+            for (int hh = 0; hh < G; ++hh) bulk_g2s(S_s + hh * ROWS * kD, tiles[hh], ROWS * kD * 4, bar);
+    }
+    if (a.pdl) pdl_wait();
+    pdl_trigger();
+    if (tid == 0 && !a.pdl_early) {
 #pragma unroll
         for (int hh = 0; hh < G; ++hh) bulk_g2s(S_s + hh * ROWS * kD, tiles[hh], ROWS * kD * 4, bar);
     }
@@ -118,16 +125,22 @@ __global__ void __launch_bounds__(256) recurrent_verify_kernel(const RecArgs a) 
     float *S_s = reinterpret_cast<float *>(smem + 128);
     float *ab = S_s + GR * kD;           // [8 warps][NV]
 
-    if (tid == 0) {
-        mbar_init(bar, 1);
-        fence_mbar_init();
-        mbar_arrive_expect_tx(bar, GR * kD * 4);
+    auto load_state = [&]() {
 #pragma unroll
         for (int hh = 0; hh < G; ++hh)
             bulk_g2s(S_s + hh * ROWS * kD,
                      a.p.state + (((size_t)r * Hv + hk * G + hh) * kD + (size_t)tile * ROWS) * kD,
                      ROWS * kD * 4, bar);
+    };
+    if (tid == 0) {
+        mbar_init(bar, 1);
+        fence_mbar_init();
+        mbar_arrive_expect_tx(bar, GR * kD * 4);
+        if (a.pdl_early) load_state();
     }
+    if (a.pdl) pdl_wait();
+    pdl_trigger();
+    if (tid == 0 && !a.pdl_early) load_state();
     __syncthreads();
     mbar_wait(bar, 0);
     float4 s[RPW];
@@ -176,6 +189,8 @@ __global__ void __launch_bounds__(256) recurrent_verify_kernel(const RecArgs a) 
 
 // Commit of the baseline: state <- temp[n_acc - 1] (Fig. 3).
 __global__ void __launch_bounds__(256) recurrent_commit_kernel(const RecArgs a) {
+    if (a.pdl) pdl_wait();
+    pdl_trigger();
     const int h = blockIdx.y, zi = blockIdx.z, r = a.first + zi;
     int na = a.nacc[zi];
     if (na < 0 || na > a.n_draft) {
@@ -197,8 +212,7 @@ static cudaError_t launch_rs(const RecArgs &a, cudaStream_t s) {
     auto kfn = recurrent_step_kernel<InT, G>;
     cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    kfn<<<dim3(kD / kRows, a.dm.Hk, a.n), 256, smem, s>>>(a);
-    return cudaGetLastError();
+    return launch_k(kfn, dim3(kD / kRows, a.dm.Hk, a.n), dim3(256), smem, s, a.pdl != 0, a);
 }
 template <int G, typename InT>
 static cudaError_t launch_rv(const RecArgs &a, cudaStream_t s) {
@@ -206,8 +220,7 @@ static cudaError_t launch_rv(const RecArgs &a, cudaStream_t s) {
     auto kfn = recurrent_verify_kernel<InT, G>;
     cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    kfn<<<dim3(kD / kRows, a.dm.Hk, a.n), 256, smem, s>>>(a);
-    return cudaGetLastError();
+    return launch_k(kfn, dim3(kD / kRows, a.dm.Hk, a.n), dim3(256), smem, s, a.pdl != 0, a);
 }
 
 template <typename InT>
@@ -236,8 +249,7 @@ cudaError_t launch_recurrent_verify(const RecArgs &a, cudaStream_t s, int64_t *l
 }
 cudaError_t launch_recurrent_commit(const RecArgs &a, cudaStream_t s, int64_t *launches) {
     if (a.n <= 0) return cudaSuccess;
-    recurrent_commit_kernel<<<dim3(8, a.dm.Hv, a.n), 256, 0, s>>>(a);
-    cudaError_t e = cudaGetLastError();
+    cudaError_t e = launch_k(recurrent_commit_kernel, dim3(8, a.dm.Hv, a.n), dim3(256), 0, s, a.pdl != 0, a);
     if (e == cudaSuccess) ++*launches;
     return e;
 }

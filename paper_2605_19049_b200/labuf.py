@@ -30,8 +30,8 @@ _STATUS_NAMES = {0: "LA_OK", 1: "LA_ERR_INVALID", 2: "LA_ERR_UNSUPPORTED", 3: "L
 EXPORTS = (
     "la_buf_query", "la_buf_create", "la_buf_destroy", "la_request_reset", "la_decode_step",
     "la_flush", "la_verify_drafts", "la_commit_accepted", "la_direct_short", "la_prefill",
-    "la_recurrent_step", "la_recurrent_verify", "la_recurrent_commit", "la_state_get",
-    "la_state_set", "la_slot_info", "la_device_status", "la_kernel_launches", "la_last_error",
+    "la_recurrent_step", "la_recurrent_verify", "la_recurrent_commit", "la_set_overlap",
+    "la_state_get", "la_state_set", "la_slot_info", "la_device_status", "la_kernel_launches", "la_last_error",
     "la_tp_unique_id", "la_tp_init", "la_tp_allgather", "la_tp_destroy",
 )
 
@@ -86,6 +86,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "la_recurrent_step": [VP, I32, I32, VP, VP, VP, VP, VP, VP, VP],
         "la_recurrent_verify": [VP, I32, I32, I32, VP, VP, VP, VP, VP, VP, VP, VP],
         "la_recurrent_commit": [VP, I32, I32, I32, VP, VP, VP],
+        "la_set_overlap": [VP, I32],
         "la_state_get": [VP, I32, VP, VP],
         "la_state_set": [VP, I32, VP, VP],
         "la_slot_info": [VP, I32, P(I32), P(I32), P(I32), P(I32)],
@@ -284,6 +285,10 @@ class LaBuf:
         self._chk(n_accepted, torch.int32, (n,), "n_accepted")
         _check(self.lib.la_recurrent_commit(self.h, first, n, N, _ptr(n_accepted), _ptr(temp),
                                             _stream()))
+
+    def set_overlap(self, enable=True):
+        """Programmatic dependent launch for this handle's kernels (la_set_overlap)."""
+        _check(self.lib.la_set_overlap(self.h, 1 if enable else 0))
 
     def state_get(self, slot, dst=None):
         c = self.cfg
