@@ -32,6 +32,8 @@
 // levels per value); the key rows are shared out over the CTA's warps.  One block
 // barrier.  (B) The forward substitution over the new tokens with one lane
 // per d_v row, and the o / u / record stores.
+#include <cuda.h>
+
 #include <cstdlib>
 
 #include "device.cuh"
@@ -45,14 +47,20 @@ constexpr int kDirectTPC = 4;       // ... and for direct slots (the key rows do
 __host__ __device__ inline uint32_t al128(uint32_t x) { return (x + 127u) & ~127u; }
 
 struct CtaLayout {
-    uint32_t S, U, K, Gs, q, k, v, kq32, Ck, Cq, av, bv, Gn, Bn, bar, bytes;
+    uint32_t S, U, K, Gs, q, k, v, kq32, Ck, Cq, av, bv, Gn, Bn, Y, bar, bytes;
 };
 
-__host__ __device__ inline CtaLayout cta_layout(int TPC, int nt, bool has_state, int jcap, int isz, int usz) {
+// tensor-core state pass: B operand rows (k_t, q_t of every new token, zero
+// padded to the MMA N granule of 16 at M = 128)
+__host__ __device__ constexpr int tc_nmma(int nt) { return (2 * nt + 15) / 16 * 16; }
+
+__host__ __device__ inline CtaLayout cta_layout(int TPC, int nt, bool has_state, int jcap, int isz, int usz,
+                                                bool tc = false) {
     CtaLayout L;
     const int J = jcap + nt;
     uint32_t o = 0;
-    L.S = o;  o = al128(o + (has_state ? (uint32_t)(TPC * 32 * kD * 4) : 0u));
+    // (tc: 1 KiB of slack so the 128-byte-swizzled state tile starts 1024-aligned)
+    L.S = o;  o = al128(o + (has_state ? (uint32_t)(TPC * 32 * kD * 4) + (tc ? 1024u : 0u) : 0u));
     L.U = o;  o = al128(o + (uint32_t)(TPC * 32 * jcap * usz));
     L.K = o;  o = al128(o + (uint32_t)(jcap * kD * isz));
     L.Gs = o; o = al128(o + (uint32_t)(((jcap + 3) & ~3) * 4));
@@ -66,7 +74,8 @@ __host__ __device__ inline CtaLayout cta_layout(int TPC, int nt, bool has_state,
     L.bv = o; o = al128(o + (uint32_t)(has_state ? TPC * nt * 32 * 4 : 0));
     L.Gn = o; o = al128(o + (uint32_t)(nt * 4));
     L.Bn = o; o = al128(o + (uint32_t)(nt * 4));
-    L.bar = o; o += 32;
+    L.Y = o;  o = al128(o + (tc ? (uint32_t)(tc_nmma(nt) * kD * 4 * (isz == 4 ? 2 : 1)) : 0u));
+    L.bar = o; o += 64;
     L.bytes = al128(o);
     return L;
 }
@@ -152,8 +161,21 @@ __device__ __forceinline__ void team_reduce(float (&v)[V], int seg, float (&res)
     }
 }
 
-template <typename InT, typename UT, int TPC, int WPT, int NT, bool HAS_STATE, int MINB>
-__global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const ChunkArgs a) {
+// TC (multi-token kinds with a state): the state mat-vecs a_t = S0 k_t,
+// b_t = S0 q_t of all new tokens are ONE M = 128 (d_v rows) x N (k_t, q_t
+// columns) x K = 128 contraction on the tensor cores: the state tile arrives
+// by 2-D TMA in the 128-byte-swizzled K-major layout the MMA reads, the
+// tokens are staged K-major, and fp32 accuracy comes from split TF32 (the
+// MMA reads the top 19 bits; pass 2 multiplies the exact remainder
+// S0 - trunc(S0), written in place once pass 1 has read the tile; fp32
+// tokens add a pass with their own remainder).
+__device__ __forceinline__ float trunc_tf32(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
+
+template <typename InT, typename UT, int TPC, int WPT, int NT, bool HAS_STATE, int MINB, bool TC>
+__global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const ChunkArgs a,
+                                                                        const __grid_constant__ CUtensorMap tmap) {
+    static_assert(!TC || (HAS_STATE && TPC == 4 && WPT == 1), "tensor-core pass: whole head per CTA");
+    constexpr int NMMA = tc_nmma(NT);
     constexpr int NTHR = TPC * WPT * 32;
     constexpr int RPW = 32 / WPT;                // d_v rows per warp
     constexpr int V = 2 * NT;                    // reduced values per row: (k_t, q_t) dots
@@ -175,11 +197,15 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
     const int Jst = a.j0_cap + NT;               // row stride of Ck/Cq
 
     extern __shared__ __align__(1024) unsigned char smem[];
-    const CtaLayout L = cta_layout(TPC, NT, HAS_STATE, a.j0_cap, isz, usz);
+    const CtaLayout L = cta_layout(TPC, NT, HAS_STATE, a.j0_cap, isz, usz, TC);
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + L.bar);
     uint64_t *recs = full + 1;                  // second barrier: the buffered records
     int *j0_s = reinterpret_cast<int *>(smem + L.bar + 16);
-    const float *S_s = reinterpret_cast<const float *>(smem + L.S);
+    uint64_t *mmab = full + 3;                  // tensor-core pass completions
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + L.bar + 32);
+    unsigned char *S_base = smem + L.S;
+    if constexpr (TC) S_base += (1024u - (smem_u32(S_base) & 1023u)) & 1023u;
+    const float *S_s = reinterpret_cast<const float *>(S_base);
     const UT *U_s = reinterpret_cast<const UT *>(smem + L.U);
     const InT *K_s = reinterpret_cast<const InT *>(smem + L.K);
     const float *G_s = reinterpret_cast<const float *>(smem + L.Gs);
@@ -208,16 +234,29 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
     //         are still in flight.
     const uint32_t fixed_bytes = (HAS_STATE ? (uint32_t)(TPC * 32 * kD * 4) : 0u) +
                                  (uint32_t)(n_new * (2 * kD * isz + TPC * 32 * isz));
+    auto issue_state = [&]() {
+        if constexpr (TC) {   // four 128-row x 32-column boxes, 128-byte swizzle
+            const int row0 = (r * Hv + h) * kD;
+#pragma unroll
+            for (int kb = 0; kb < 4; ++kb) tma_load_2d(S_base + kb * (TPC * 32 * 128), &tmap, kb * 32, row0, full);
+        } else {
+            bulk_g2s(smem + L.S, a.p.state + (((size_t)r * Hv + h) * kD + (size_t)tile0 * 32) * kD,
+                     TPC * 32 * kD * 4, full);
+        }
+    };
+    if constexpr (TC) {
+        if (warp == 0) tmem_alloc<32>(tmem_slot);
+    }
     if (tid == 0) {
         mbar_init(full, 1);
         mbar_init(recs, 1);
+        if (TC) mbar_init(mmab, 1);
         fence_mbar_init();
         if (HAS_STATE && a.pdl_early) {
             // the state tile is not written by the grid this one overlaps
             // (launch overlap), so it streams in while that grid drains
             mbar_arrive_expect_tx(full, fixed_bytes);
-            bulk_g2s(smem + L.S, a.p.state + (((size_t)r * Hv + h) * kD + (size_t)tile0 * 32) * kD,
-                     TPC * 32 * kD * 4, full);
+            issue_state();
         }
     }
     if (a.pdl) pdl_wait();   // inputs, counters and records may come from the previous grid
@@ -233,9 +272,7 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
     if (tid == 0) {
         if (!(HAS_STATE && a.pdl_early)) {
             mbar_arrive_expect_tx(full, fixed_bytes);
-            if (HAS_STATE)
-                bulk_g2s(smem + L.S, a.p.state + (((size_t)r * Hv + h) * kD + (size_t)tile0 * 32) * kD,
-                         TPC * 32 * kD * 4, full);
+            if (HAS_STATE) issue_state();
         }
         const int j0v = (direct ? a.p.len : a.p.occ)[r] + a.j_add;
         const int jbv = (j0v + 3) & ~3;
@@ -286,6 +323,11 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
     mbar_wait(full, 0);
     if (a.dbg & 1) {
         mbar_wait(recs, 0);
+        if constexpr (TC) {
+            tc_fence_before();
+            __syncthreads();
+            if (warp == 0) tmem_dealloc<32>(*tmem_slot);
+        }
         if (a.kind != CK_VERIFY && tid == 0 && ticket == (int)(gridDim.x * gridDim.y) - 1) {
             a.p.ticket[r] = 0;
             const int Jd = *j0_s + n_new;
@@ -306,6 +348,45 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
             kq32[(t * 2 + 1) * kD + c] = to_f(q_s[e]);
         }
         __syncthreads();
+    }
+    uint32_t tmem = 0;
+    float *Yh = reinterpret_cast<float *>(smem + L.Y);
+    float *Yl = Yh + NMMA * kD;
+    auto mma_pass = [&](const float *Y, bool acc) {
+        const uint32_t idesc = idesc_tf32(128, NMMA);
+#pragma unroll
+        for (int kk = 0; kk < kD / 8; ++kk) {
+            const uint64_t da = umma_desc_sw128(smem_u32(S_base) + (kk >> 2) * (TPC * 32 * 128) + (kk & 3) * 32);
+            const uint64_t db = umma_desc_noswz(smem_u32(Y) + kk * 256, 128, kD * 32);
+            tc_mma_tf32(tmem, da, db, idesc, (acc || kk > 0) ? 1u : 0u);
+        }
+    };
+    if constexpr (TC) {
+        // B operand: row n = (k_t | q_t) of token n / 2, K-major SWIZZLE_NONE
+        // (8-row x 16-byte core matrices, K-adjacent at +128 B, row groups at +4 KiB)
+        for (int e = tid; e < NMMA * kD; e += NTHR) {
+            const int n = e / kD, c = e % kD, t = n >> 1;
+            float x = 0.f;
+            if (t < n_new) x = to_f(((n & 1) ? q_s : k_s)[t * kD + c]);
+            const int off = (n >> 3) * (kD * 32 / 4) + (c >> 2) * 32 + (n & 7) * 4 + (c & 3);
+            if constexpr (isz == 4) {
+                const float hi = trunc_tf32(x);
+                Yh[off] = hi;
+                Yl[off] = x - hi;
+            } else {
+                Yh[off] = x;     // bf16 values are exact in tf32
+            }
+        }
+        fence_proxy_async_smem();
+        tc_fence_before();
+        __syncthreads();
+        tc_fence_after();
+        tmem = *tmem_slot;
+        if (tid == 0) {
+            mma_pass(Yh, false);                    // trunc(S0) . Y_hi
+            if constexpr (isz == 4) mma_pass(Yl, true);   // trunc(S0) . Y_lo
+            tc_commit(mmab);
+        }
     }
     int j0 = 0, J = 0;
     float gn_l = 0.f;
@@ -337,9 +418,13 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
                 }
             }
         };
-        // state rows of the warp's tile: 4 steps of 8 rows
-        if constexpr (HAS_STATE) {
-#pragma unroll(NT == 1 ? 4 : 1)
+        // state rows of the warp's tile: 4 steps of 8 rows (one token), or --
+        // when k_t / q_t come from shared memory (several tokens) -- 2 steps
+        // of 2 x 8 rows, so every k_t / q_t chunk load serves two rows
+        if constexpr (TC) {
+            // (the tensor-core pass is in flight; see after the key rows)
+        } else if constexpr (HAS_STATE && KQ_REG) {
+#pragma unroll 4
             for (int st = 0; st < RPW / 8; ++st) {
                 const int rf = half * RPW + st * 8 + team;
                 float4 x[8];
@@ -353,6 +438,37 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
                 for (int o = 0; o < NOUT; ++o) {
                     const int t = xid[o] >> 1;
                     if (xid[o] >= 0 && t < n_new) ((xid[o] & 1) ? bv : av)[(wt * NT + t) * 32 + rf] = res[o];
+                }
+            }
+        } else if constexpr (HAS_STATE) {
+            static_assert(RPW % 16 == 0, "two row blocks per step");
+            constexpr int NOUT2 = TeamOut<2 * V>::N;
+            for (int st = 0; st < RPW / 16; ++st) {
+                const int rf0 = half * RPW + st * 16 + team, rf1 = rf0 + 8;
+                float4 x0[8], x1[8];
+                load_row8(S_s + (size_t)(wt * 32 + rf0) * kD, seg, par, x0);
+                load_row8(S_s + (size_t)(wt * 32 + rf1) * kD, seg, par, x1);
+                float vals[2 * V];
+#pragma unroll
+                for (int t = 0; t < NT; ++t) {
+                    float4 y[8];
+                    if constexpr (KQ32) load_row8(kq32 + (size_t)(t * 2) * kD, seg, par, y);
+                    else load_row8(k_s + (size_t)t * kD, seg, par, y);
+                    vals[2 * t] = dot8x4(x0, y);
+                    vals[V + 2 * t] = dot8x4(x1, y);
+                    if constexpr (KQ32) load_row8(kq32 + (size_t)(t * 2 + 1) * kD, seg, par, y);
+                    else load_row8(q_s + (size_t)t * kD, seg, par, y);
+                    vals[2 * t + 1] = dot8x4(x0, y);
+                    vals[V + 2 * t + 1] = dot8x4(x1, y);
+                }
+                float res[NOUT2];
+                int xid[NOUT2];
+                team_reduce<2 * V>(vals, seg, res, xid);
+#pragma unroll
+                for (int o = 0; o < NOUT2; ++o) {
+                    const int xv = xid[o] % V, rf = xid[o] < V ? rf0 : rf1;
+                    const int t = xv >> 1;
+                    if (xid[o] >= 0 && t < n_new) ((xv & 1) ? bv : av)[(wt * NT + t) * 32 + rf] = res[o];
                 }
             }
         }
@@ -397,13 +513,53 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
             }
         }
     }
+    if constexpr (TC) {
+        // pass 2 on the exact remainder S0 - trunc(S0), written in place once
+        // pass 1 has read the tile (the split is elementwise: layout-agnostic)
+        mbar_wait(mmab, 0);
+        float4 *S4 = reinterpret_cast<float4 *>(S_base);
+        for (int e = tid; e < TPC * 32 * kD / 4; e += NTHR) {
+            float4 x = S4[e];
+            x.x -= trunc_tf32(x.x);
+            x.y -= trunc_tf32(x.y);
+            x.z -= trunc_tf32(x.z);
+            x.w -= trunc_tf32(x.w);
+            S4[e] = x;
+        }
+        fence_proxy_async_smem();
+        __syncthreads();
+        if (tid == 0) {
+            tc_fence_after();
+            mma_pass(Yh, true);                     // (S0 - trunc(S0)) . Y_hi
+            tc_commit(mmab);
+        }
+        mbar_wait(mmab, 1);
+        tc_fence_after();
+        // D row m = d_v row 32 w + lane: warp w reads TMEM lanes 32w..32w+31
+        float dv[32];
+        tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16), dv);
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+            if (t < n_new) {
+                av[(warp * NT + t) * 32 + lane] = dv[2 * t];
+                bv[(warp * NT + t) * 32 + lane] = dv[2 * t + 1];
+            }
+        }
+    }
     if (dm.validate) {
         for (int e = tid; e < n_new * kD; e += NTHR) {
             const float kk = to_f(k_s[e]), qq = to_f(q_s[e]);
             if (!(isfinite(kk) && isfinite(qq))) bad |= 0x4u;
         }
     }
+    if constexpr (TC) tc_fence_before();
     __syncthreads();
+    if constexpr (TC) {
+        if (warp == 0) {
+            tc_fence_after();
+            tmem_dealloc<32>(tmem);
+        }
+    }
 
     // ---- 3. forward substitution over the new tokens.  Lane -> d_v row
     //         (half * RPW + lane % RPW) of the warp's tile; the WPT lanes of a
@@ -489,31 +645,43 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
 }
 
 // ---------------------------------------------------------------- launch
-template <typename InT, typename UT, int TPC, int WPT, int NT, bool HAS_STATE>
+template <typename InT, typename UT, int TPC, int WPT, int NT, bool HAS_STATE, int MBO = 0, bool TC = false>
 static cudaError_t launch_cfg(const ChunkArgs &a, cudaStream_t s) {
-    const CtaLayout L = cta_layout(TPC, NT, HAS_STATE, a.j0_cap, sizeof(InT), sizeof(UT));
+    const CtaLayout L = cta_layout(TPC, NT, HAS_STATE, a.j0_cap, sizeof(InT), sizeof(UT), TC);
     if (L.bytes > 227 * 1024) return cudaErrorInvalidConfiguration;
-    constexpr int MINB = NT <= 2 ? (HAS_STATE ? 12 / (TPC * WPT) : 2) : 1;
-    auto kfn = chunk_cta_kernel<InT, UT, TPC, WPT, NT, HAS_STATE, MINB < 1 ? 1 : MINB>;
+    constexpr int MINB = MBO ? MBO : (NT <= 2 ? (HAS_STATE ? 12 / (TPC * WPT) : 2) : 1);
+    auto kfn = chunk_cta_kernel<InT, UT, TPC, WPT, NT, HAS_STATE, MINB < 1 ? 1 : MINB, TC>;
     cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.bytes);
     if (e != cudaSuccess) return e;
-    return launch_k(kfn, dim3(4 / TPC, a.dm.Hv, a.n), dim3(TPC * WPT * 32), L.bytes, s, a.pdl != 0, a);
+    CUtensorMap tm;
+    if (TC) tm = *static_cast<const CUtensorMap *>(a.tmap);
+    else memset(&tm, 0, sizeof(tm));
+    return launch_k(kfn, dim3(4 / TPC, a.dm.Hv, a.n), dim3(TPC * WPT * 32), L.bytes, s, a.pdl != 0, a, tm);
 }
 
-template <typename InT, typename UT, int TPC, int WPT, bool HAS_STATE>
+template <typename InT, typename UT, int TPC, int WPT, bool HAS_STATE, int MBO = 0, bool TC = false>
 static cudaError_t launch_nt(const ChunkArgs &a, cudaStream_t s) {
-    if (a.n_new == 1) return launch_cfg<InT, UT, TPC, WPT, 1, HAS_STATE>(a, s);
-    if (a.n_new <= 2) return launch_cfg<InT, UT, TPC, WPT, 2, HAS_STATE>(a, s);
-    if (a.n_new <= 4) return launch_cfg<InT, UT, TPC, WPT, 4, HAS_STATE>(a, s);
-    if (a.n_new <= 8) return launch_cfg<InT, UT, TPC, WPT, 8, HAS_STATE>(a, s);
-    return launch_cfg<InT, UT, TPC, WPT, 16, HAS_STATE>(a, s);
+    if (!TC && a.n_new == 1) return launch_cfg<InT, UT, TPC, WPT, 1, HAS_STATE, MBO, TC>(a, s);
+    if (a.n_new <= 2) return launch_cfg<InT, UT, TPC, WPT, 2, HAS_STATE, MBO, TC>(a, s);
+    if (a.n_new <= 4) return launch_cfg<InT, UT, TPC, WPT, 4, HAS_STATE, MBO, TC>(a, s);
+    if (a.n_new <= 8) return launch_cfg<InT, UT, TPC, WPT, 8, HAS_STATE, MBO, TC>(a, s);
+    return launch_cfg<InT, UT, TPC, WPT, 16, HAS_STATE, MBO, TC>(a, s);
 }
 
 template <typename InT, typename UT>
 static cudaError_t launch_t(const ChunkArgs &a, cudaStream_t s) {
     // (1 or 4 tiles per CTA and 2 warps per tile were measured and rejected,
     //  DESIGN.md section 6)
-    if (a.kind == CK_DIRECT) return launch_nt<InT, UT, kDirectTPC, 1, false>(a, s);
+    // direct: at most 128 registers so 4 CTAs (16 warps) share an SM (measured
+    // 338 -> 281 us at config 4; 5 CTAs spill more and lose); 2 warps per tile
+    // for the multi-token kinds was measured slower (195 -> 262-280 us)
+    if (a.kind == CK_DIRECT) return launch_nt<InT, UT, kDirectTPC, 1, false, 4>(a, s);
+    // 8 or more new tokens (verify with N >= 8, prefill chunks): the state
+    // mat-vecs on the tensor cores, one CTA per (slot, V head).  Measured at
+    // batch 256 (tools/time_verify.py): N = 2 / 4 / 8 -> 197 / 224 / 290 us
+    // vs 107 / 189 / 322 us on the CUDA cores.  LABUF_TC=0 forces CUDA cores.
+    static const int tc_env = getenv("LABUF_TC") ? atoi(getenv("LABUF_TC")) : 8;
+    if (tc_env && a.n_new >= tc_env && a.n_new >= 2 && a.tmap) return launch_nt<InT, UT, 4, 1, true, 1, true>(a, s);
     return launch_nt<InT, UT, kChunkTPC, 1, true>(a, s);
 }
 

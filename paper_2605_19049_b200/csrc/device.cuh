@@ -131,10 +131,10 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 // the previous kernel on the stream when pdl (its CTAs may start while that
 // kernel drains; everything the kernel reads that another grid may write
 // must come after pdl_wait()).
-template <typename Kern, typename Arg>
-inline cudaError_t launch_k(Kern kfn, dim3 g, dim3 b, size_t smem, cudaStream_t s, bool pdl, const Arg &arg) {
+template <typename Kern, typename... Arg>
+inline cudaError_t launch_k(Kern kfn, dim3 g, dim3 b, size_t smem, cudaStream_t s, bool pdl, const Arg &...arg) {
     if (!pdl) {
-        kfn<<<g, b, smem, s>>>(arg);
+        kfn<<<g, b, smem, s>>>(arg...);
         return cudaGetLastError();
     }
     cudaLaunchConfig_t cfg = {};
@@ -147,7 +147,7 @@ inline cudaError_t launch_k(Kern kfn, dim3 g, dim3 b, size_t smem, cudaStream_t 
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, kfn, arg);
+    return cudaLaunchKernelEx(&cfg, kfn, arg...);
 }
 
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
@@ -221,6 +221,25 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
     for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// 2-D TMA tile load (tensor map in kernel-parameter space) onto an mbarrier.
+__device__ __forceinline__ void tma_load_2d(void *dst_smem, const void *tmap, int c0, int c1, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+        ::"r"(smem_u32(dst_smem)), "l"(tmap), "r"(c0), "r"(c1), "r"(smem_u32(bar)) : "memory");
+}
+// UMMA descriptor, K-major SWIZZLE_128B (the layout a 128-byte-wide TMA box
+// with CU_TENSOR_MAP_SWIZZLE_128B writes): 8-row x 128-byte atoms, 1024 B
+// apart; K steps inside an atom advance the start address.
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t smem_addr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((smem_addr >> 4) & 0x3FFFu);
+    d |= (uint64_t)1 << 16;                    // lbo (unused for swizzled K-major)
+    d |= (uint64_t)(1024 >> 4) << 32;          // sbo: 8-row groups
+    d |= (uint64_t)1 << 46;                    // version 1 (sm_100)
+    d |= (uint64_t)2 << 61;                    // layout SWIZZLE_128B
+    return d;
 }
 
 // UMMA shared-memory matrix descriptor, SWIZZLE_NONE (canonical K-major

@@ -5,6 +5,8 @@
 // except la_device_status.
 #include "../../include/la.h"
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -19,6 +21,7 @@
 using namespace labuf;
 
 namespace {
+
 
 thread_local std::string g_last_error;
 
@@ -55,9 +58,46 @@ struct la_buf {
     std::vector<int32_t> occ, len, mode, pending;   // host mirror
     int64_t launches = 0;
     int overlap = 0;                                 // la_set_overlap
+    alignas(64) unsigned char tmap[128];             // CUtensorMap of the state (tensor-core pass)
+    int tmap_state = 0;                              // 0 not built, 1 ok, 2 unavailable
 };
 
 namespace {
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void *ptr = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+    }
+    return fn;
+}
+
+// The state viewed as a 2-D fp32 tensor [R*Hv*128 rows][128], read in
+// 128-row x 32-column boxes with the 128-byte swizzle the tensor-core pass
+// of kernels (3)/prefill consumes.  Built once per handle, on first use.
+const void *state_tmap(la_buf *b) {
+    if (b->tmap_state == 0) {
+        b->tmap_state = 2;
+        if (auto enc = tmap_encoder()) {
+            const cuuint64_t dims[2] = {(cuuint64_t)kD, (cuuint64_t)b->dm.R * b->dm.Hv * kD};
+            const cuuint64_t strides[1] = {(cuuint64_t)kD * 4};
+            const cuuint32_t box[2] = {32, 128};
+            const cuuint32_t estr[2] = {1, 1};
+            if (enc(reinterpret_cast<CUtensorMap *>(b->tmap), CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, b->p.state,
+                    dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
+                b->tmap_state = 1;
+        }
+    }
+    return b->tmap_state == 1 ? b->tmap : nullptr;
+}
 
 // The library's last kernel launch on this host thread: whose state it was,
 // on which stream, and whether it wrote that state.  A launch with overlap
@@ -185,6 +225,7 @@ cudaError_t run_chunk(la_buf *b, int first, int n, int n_tok, int j0_cap, int to
             a.beta = beta + sq * b->dm.Hv;
             a.o = o ? o + sq * b->dm.Hv * d : nullptr;
             overlap_flags(b, s, a);
+            a.tmap = (kind == CK_VERIFY || kind == CK_PREFILL) && m >= 2 ? state_tmap(b) : nullptr;
             cudaError_t e = launch_chunk(a, s, &b->launches);
             if (e != cudaSuccess) return e;
             note_launch(b, s, false);
