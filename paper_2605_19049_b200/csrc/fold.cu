@@ -71,7 +71,7 @@ __device__ __forceinline__ uint32_t kmaj_off(int row, int k, int kc) {
 // i.e. U = T Diag(beta) (V - Diag(e^G) W) with T = [I + strictLower(Diag(beta)
 // (Gamma (.) K K^T))]^{-1}, then the same tensor-core fold as mode i.
 template <typename InT, typename UT, bool FP32_IN, int kFoldNJ, int KCM, bool RAW>
-__global__ void __launch_bounds__(kFoldThreads, RAW ? 4 : (kFoldNJ == 32 && KCM == 16 ? 8 : 4)) fold_kernel(const FoldArgs a) {
+__global__ void __launch_bounds__(kFoldThreads, RAW ? 4 : (kFoldNJ == 128 ? 2 : (kFoldNJ == 32 && KCM == 16 ? 8 : 4))) fold_kernel(const FoldArgs a) {
     constexpr int NPAR = kFoldThreads / kFoldNJ;   // token parities per B row
     const int jh = blockIdx.x, h = blockIdx.y, zi = blockIdx.z;
     const int r = a.first + zi;
@@ -416,11 +416,21 @@ static cudaError_t launch_fold_cfg(const FoldArgs &a, cudaStream_t s) {
 
 template <typename InT, typename UT, bool FP32_IN>
 static cudaError_t launch_fold_t(const FoldArgs &a, cudaStream_t s) {
-    // LABUF_FOLD_NJ: d_v rows per CTA (32 or 64; tuning sweeps)
-    static const int nj = getenv("LABUF_FOLD_NJ") ? atoi(getenv("LABUF_FOLD_NJ")) : 32;
+    // d_v rows per CTA.  Every CTA of a TMEM-allocating kernel costs ~0.5 us
+    // of SM-serialised launch/allocation time on B200 (tools/microbench_tmem.cu:
+    // 3.7 ns per CTA GPU-wide vs 0.64 ns for a plain kernel), so launches where
+    // many CTAs fold little or nothing (commits: zero or few accepted drafts)
+    // take 64-row CTAs (half the CTAs): config-3 commit 164 -> 127 us.  Full
+    // flushes keep 32-row CTAs (more CTAs per SM in flight): 57 vs 62 us.
+    // LABUF_FOLD_NJ=32/64/128 forces one size (tuning sweeps).
+    static const int nj_env = getenv("LABUF_FOLD_NJ") ? atoi(getenv("LABUF_FOLD_NJ")) : 0;
+    const int nj = nj_env ? nj_env : (a.spec ? 32 : 64);
     if (a.raw)
         return a.kc <= 16 ? launch_fold_cfg<InT, UT, FP32_IN, 32, 16, true>(a, s)
                           : launch_fold_cfg<InT, UT, FP32_IN, 32, 32, true>(a, s);
+    if (nj == 128)
+        return a.kc <= 16 ? launch_fold_cfg<InT, UT, FP32_IN, 128, 16, false>(a, s)
+                          : launch_fold_cfg<InT, UT, FP32_IN, 128, 32, false>(a, s);
     if (nj == 64)
         return a.kc <= 16 ? launch_fold_cfg<InT, UT, FP32_IN, 64, 16, false>(a, s)
                           : launch_fold_cfg<InT, UT, FP32_IN, 64, 32, false>(a, s);
