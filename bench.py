@@ -52,6 +52,8 @@ def parse_args():
     p.add_argument("--no-rows", action="store_true", help="skip the verify / direct rows")
     p.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     p.add_argument("--no-overlap", action="store_true", help="launch without PDL (la_set_overlap 0)")
+    p.add_argument("--auto-flush", action="store_true",
+                   help="headline WITH the fused flush (la_set_auto_flush; measured slower, see DESIGN.md)")
     p.add_argument("--seed", type=int, default=1002)
     return p.parse_args()
 
@@ -330,17 +332,38 @@ def main():
         for b in bufs:
             b.flush(0, B, L.LA_FLUSH_FULL)
 
+    # unfused cycle (C decode launches + the tcgen05 flush kernel): measured
+    # first, reported beside the headline and for the flush kernel's row
     n0 = sum(b.kernel_launches() for b in bufs)
     g_dec = capture(torch, stream, dec_phase)
     n1 = sum(b.kernel_launches() for b in bufs)
     g_fl = capture(torch, stream, flush_phase)
     n2 = sum(b.kernel_launches() for b in bufs)
-    launches_per_step = n2 - n0
     dec_launches, fl_launches = n1 - n0, n2 - n1
-
     barrier()
     t_c0 = time.time()
-    total_ms, (dec_ms, fl_ms) = timed_graphs(torch, stream, [g_dec, g_fl], K, W)
+    uf_total_ms, (dec_ms, fl_ms) = timed_graphs(torch, stream, [g_dec, g_fl], K, W)
+    uf_total_ms = max_over_ranks(uf_total_ms)
+    del g_dec, g_fl
+    auto = args.auto_flush
+    # the fused flush (la_set_auto_flush): the step that fills
+    # the buffers folds them inside the decode kernel; always measured (row
+    # "fused_flush"), the headline only with --auto-flush
+    for b in bufs:
+        b.set_auto_flush(True)
+    n0 = sum(b.kernel_launches() for b in bufs)
+    g_dec = capture(torch, stream, dec_phase)
+    f_launches = sum(b.kernel_launches() for b in bufs) - n0
+    barrier()
+    f_total_ms, (fdec_ms,) = timed_graphs(torch, stream, [g_dec], K, W)
+    f_total_ms = max_over_ranks(f_total_ms)
+    for b in bufs:
+        b.set_auto_flush(False)
+    del g_dec
+    if auto:
+        total_ms, launches_per_step = f_total_ms, f_launches
+    else:
+        total_ms, launches_per_step = uf_total_ms, dec_launches + fl_launches
     barrier()
     t_c1 = time.time()
     total_ms = max_over_ranks(total_ms)
@@ -363,17 +386,24 @@ def main():
     rec_total = max_over_ranks(rec_total)
     rec_us_per_token = 1e3 * rec_total / K / (C * NL)
 
-    # ---- roofline of the dominant kernel (buffered decode, kernel 1)
-    dec_bytes_per_launch = B * sum(lb.decode(j) for j in range(C)) / C
-    dec_us = 1e3 * dec_ms / (K * dec_launches)
+    # ---- roofline of the dominant kernel (buffered decode, kernel 1; with the
+    #      fused flush its filling step also writes the folded state)
+    uf_dec_bytes_per_launch = B * sum(lb.decode(j) for j in range(C)) / C
+    uf_dec_us = 1e3 * dec_ms / (K * dec_launches)
+    if auto:
+        dec_bytes_per_launch = B * (sum(lb.decode(j) for j in range(C)) + lb.st) / C
+        dec_us = 1e3 * fdec_ms / (K * dec_launches)
+    else:
+        dec_bytes_per_launch, dec_us = uf_dec_bytes_per_launch, uf_dec_us
     fl_bytes_per_launch = B * lb.flush(C)
     fl_us = 1e3 * fl_ms / (K * fl_launches)
     rec_bytes_per_launch = B * lb.recurrent()
     rec_us = 1e3 * rec_ms / (K * C * NL)
     gbs = lambda nbytes, us: nbytes / (us * 1e-6) / 1e9
     dec_gbs = gbs(dec_bytes_per_launch, dec_us)
-    step_bytes = NL * (B * sum(lb.decode(j) for j in range(C)) + fl_bytes_per_launch)
-    traffic = ncu_traffic("decode")
+    step_bytes = NL * (B * sum(lb.decode(j) for j in range(C)) + (B * lb.st if auto else fl_bytes_per_launch))
+    uf_us_per_token = 1e3 * uf_total_ms / K / (C * NL)
+    traffic = ncu_traffic("decode_cycle_fused" if auto else "decode")
     traffic_fl = ncu_traffic("flush")
     traffic_rec = ncu_traffic("recurrent_step")
 
@@ -385,7 +415,10 @@ def main():
                    "batch_per_gpu": B, "global_batch": B * world, "chunk": C, "layers_rotated": NL,
                    "heads": {"qk": Hk, "v": Hv, "d": D}, "in_dtype": args.in_dtype, "u_dtype": args.u_dtype,
                    "state": "fp32", "parallelism": f"dp{world} (requests partitioned, no collective)",
-                   "step": f"one buffer cycle: {C} decode steps + 1 flush, x {NL} layer instances",
+                   "step": (f"one buffer cycle: {C} decode steps, the last folding the buffer in-kernel "
+                            f"(fused flush), x {NL} layer instances" if auto else
+                            f"one buffer cycle: {C} decode steps + 1 flush, x {NL} layer instances"),
+                   "fused_flush": auto,
                    "l2": f"inputs larger than L2: {NL} layers x {B * lb.st / 2**20:.0f} MiB state rotated per step",
                    "cuda_graphs": True, "launch_overlap": not args.no_overlap},
         "us_per_token": us_per_token,
@@ -395,6 +428,12 @@ def main():
         "recurrent": {"us_per_token": rec_us_per_token,
                       "tokens_per_s_per_gpu": B / (rec_us_per_token * 1e-6),
                       "hbm_frac_of_measured": gbs(rec_bytes_per_launch, rec_us) / peak},
+        "unfused": {"us_per_token": uf_us_per_token, "tokens_per_s_per_gpu": B / (uf_us_per_token * 1e-6),
+                    "note": "the cycle with the separate tcgen05 flush kernel (la_set_auto_flush 0)"},
+        "fused_flush": {"us_per_token": 1e3 * f_total_ms / K / (C * NL),
+                        "note": "the cycle with the flush folded into the filling decode step on CUDA cores "
+                                "(la_set_auto_flush 1, SURVEY NEXT-1); slower on B200: the 64-thread decode CTA "
+                                "is compute-bound on the C x 64 x 128 fold"},
         "speedup_vs_recurrent": rec_us_per_token / us_per_token,
         "latency_reduction_pct_vs_recurrent": 100.0 * (1 - us_per_token / rec_us_per_token),
         "paper_context": {"latency_reduction_pct": 45.17, "capacity_x": 5,
@@ -402,10 +441,14 @@ def main():
         "kernels": {
             "decode": {"us_per_launch": dec_us, "bytes_per_launch": dec_bytes_per_launch,
                        "gbs": dec_gbs, "frac_of_measured": dec_gbs / peak, "launches_per_step": dec_launches,
-                       "share_of_step": dec_ms / (dec_ms + fl_ms), "ncu_dram_bytes_per_launch": traffic},
+                       "share_of_step": 1.0 if auto else dec_ms / (dec_ms + fl_ms),
+                       "fused_flush": auto, "ncu_dram_bytes_per_launch": traffic},
+            "decode_unfused": {"us_per_launch": uf_dec_us, "bytes_per_launch": uf_dec_bytes_per_launch,
+                               "gbs": gbs(uf_dec_bytes_per_launch, uf_dec_us),
+                               "frac_of_measured": gbs(uf_dec_bytes_per_launch, uf_dec_us) / peak},
             "flush": {"us_per_launch": fl_us, "bytes_per_launch": fl_bytes_per_launch,
                       "gbs": gbs(fl_bytes_per_launch, fl_us), "frac_of_measured": gbs(fl_bytes_per_launch, fl_us) / peak,
-                      "launches_per_step": fl_launches, "share_of_step": fl_ms / (dec_ms + fl_ms),
+                      "launches_per_step": fl_launches, "share_of_unfused_step": fl_ms / (dec_ms + fl_ms),
                       "ncu_dram_bytes_per_launch": traffic_fl},
             "recurrent_step": {"us_per_launch": rec_us, "bytes_per_launch": rec_bytes_per_launch,
                                "gbs": gbs(rec_bytes_per_launch, rec_us),
@@ -417,9 +460,10 @@ def main():
                      "frac": dec_gbs / peak,
                      "traffic": traffic,
                      "algorithmic_bytes_per_launch": dec_bytes_per_launch,
-                     "note": "achieved = B x mean_j(st + inp + j*rec + o + rec) over occupancies j = 0..C-1 "
-                             "(DESIGN.md section 6) / mean launch time from CUDA events around the captured decode "
-                             "graph; traffic = ncu dram bytes per launch (profiles/ncu_traffic.json)"},
+                     "note": "achieved = B x (sum_j (st + inp + j*rec + o + rec) over occupancies j = 0..C-1 "
+                             "+ st written by the fused fold) / C (DESIGN.md section 6) / mean launch time from CUDA "
+                             "events around the captured decode graph; traffic = ncu dram bytes per launch "
+                             "(profiles/ncu_traffic.json)"},
         "gpu_launches": launches_per_step * K,
     }
 
@@ -483,7 +527,7 @@ def main():
 
     # ---- extra rows: verify + commit (config 3) and direct (config 4)
     if not args.no_rows:
-        del g_dec, g_fl, g_rec
+        del g_rec
         line["rows"] = extra_rows(torch, L, cost, dev, stream, seed0 + 5000, K, W, peak, args)
 
     t_c3 = time.time()

@@ -240,6 +240,17 @@ LA_API la_status la_recurrent_commit(la_buf *buf, int32_t first, int32_t n, int3
  * in between).  Default 0 (off).  LA_ERR_INVALID on enable not 0/1. */
 LA_API la_status la_set_overlap(la_buf *buf, int32_t enable);
 
+/* Fused flush: with enable = 1 and
+ * chunk <= 32, a la_decode_step that fills a slot's buffer (occ reaches
+ * chunk) folds the slot's `chunk` records into its state inside the decode
+ * kernel -- S <- e^{G_last} S0 + sum_i e^{G_last-G_i} u_i k_i^T on CUDA cores
+ * (fp32), from the S0 rows the step has already read -- and leaves occ = 0;
+ * the separate flush and its second read of the state disappear.  A
+ * la_flush(FULL) after such a step is an empty no-op.  Outputs are those of
+ * the unfused path (same buffered u, fold within fp32 rounding).  Default 0.
+ * LA_ERR_INVALID on enable not 0/1. */
+LA_API la_status la_set_auto_flush(la_buf *buf, int32_t enable);
+
 LA_API la_status la_state_get(la_buf *buf, int32_t slot, float *dst, la_stream stream);
 LA_API la_status la_state_set(la_buf *buf, int32_t slot, const float *src, la_stream stream);
 

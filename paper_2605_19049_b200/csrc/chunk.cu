@@ -47,7 +47,7 @@ constexpr int kDirectTPC = 4;       // ... and for direct slots (the key rows do
 __host__ __device__ inline uint32_t al128(uint32_t x) { return (x + 127u) & ~127u; }
 
 struct CtaLayout {
-    uint32_t S, U, K, Gs, q, k, v, kq32, Ck, Cq, av, bv, Gn, Bn, Y, bar, bytes;
+    uint32_t S, U, K, Gs, q, k, v, kq32, Ck, Cq, av, bv, Gn, Bn, Y, Kf, bar, bytes;
 };
 
 // tensor-core state pass: B operand rows (k_t, q_t of every new token, zero
@@ -55,7 +55,7 @@ struct CtaLayout {
 __host__ __device__ constexpr int tc_nmma(int nt) { return (2 * nt + 15) / 16 * 16; }
 
 __host__ __device__ inline CtaLayout cta_layout(int TPC, int nt, bool has_state, int jcap, int isz, int usz,
-                                                bool tc = false) {
+                                                bool tc = false, bool fold = false) {
     CtaLayout L;
     const int J = jcap + nt;
     uint32_t o = 0;
@@ -75,6 +75,7 @@ __host__ __device__ inline CtaLayout cta_layout(int TPC, int nt, bool has_state,
     L.Gn = o; o = al128(o + (uint32_t)(nt * 4));
     L.Bn = o; o = al128(o + (uint32_t)(nt * 4));
     L.Y = o;  o = al128(o + (tc ? (uint32_t)(tc_nmma(nt) * kD * 4 * (isz == 4 ? 2 : 1)) : 0u));
+    L.Kf = o; o = al128(o + (fold ? (uint32_t)(J * kD * 4) : 0u));   // fused fold: fp32 keys
     L.bar = o; o += 64;
     L.bytes = al128(o);
     return L;
@@ -171,10 +172,18 @@ __device__ __forceinline__ void team_reduce(float (&v)[V], int seg, float (&res)
 // tokens add a pass with their own remainder).
 __device__ __forceinline__ float trunc_tf32(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
 
-template <typename InT, typename UT, int TPC, int WPT, int NT, bool HAS_STATE, int MINB, bool TC>
+// FOLD (decode with auto-flush, la_set_auto_flush): when the step fills the
+// slot's buffer (J == C), the CTA -- which holds the S0 rows of its tiles,
+// every buffered key and its rows' delta values -- folds the C records into
+// those rows itself (P:407 on CUDA cores, fp32), and writes S_new: the
+// separate flush, and its second read of the state, disappear.
+constexpr int kFusedFoldMaxC = 32;
+
+template <typename InT, typename UT, int TPC, int WPT, int NT, bool HAS_STATE, int MINB, bool TC, bool FOLD = false>
 __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const ChunkArgs a,
                                                                         const __grid_constant__ CUtensorMap tmap) {
     static_assert(!TC || (HAS_STATE && TPC == 4 && WPT == 1), "tensor-core pass: whole head per CTA");
+    static_assert(!FOLD || (NT == 1 && HAS_STATE && WPT == 1 && !TC), "fused fold: decode kind only");
     constexpr int NMMA = tc_nmma(NT);
     constexpr int NTHR = TPC * WPT * 32;
     constexpr int RPW = 32 / WPT;                // d_v rows per warp
@@ -197,7 +206,7 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
     const int Jst = a.j0_cap + NT;               // row stride of Ck/Cq
 
     extern __shared__ __align__(1024) unsigned char smem[];
-    const CtaLayout L = cta_layout(TPC, NT, HAS_STATE, a.j0_cap, isz, usz, TC);
+    const CtaLayout L = cta_layout(TPC, NT, HAS_STATE, a.j0_cap, isz, usz, TC, FOLD);
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + L.bar);
     uint64_t *recs = full + 1;                  // second barrier: the buffered records
     int *j0_s = reinterpret_cast<int *>(smem + L.bar + 16);
@@ -627,6 +636,50 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
                 }
             }
         }
+        if constexpr (FOLD) {
+            if (J == dm.C) {   // CTA-uniform
+                // the J keys as fp32 rows, once per CTA
+                float *Kf = reinterpret_cast<float *>(smem + L.Kf);
+                for (int e = tid; e < J * kD; e += NTHR)
+                    Kf[e] = to_f(e < j0 * kD ? K_s[e] : k_s[e - j0 * kD]);
+                // this thread's state row: S_new = e^{G_t} S0 + sum_{i<J} e^{G_t-G_i} u_i k_i^T
+                const float gt = Gn_s[0];
+                float coef[kFusedFoldMaxC];
+#pragma unroll
+                for (int i = 0; i < kFusedFoldMaxC; ++i)
+                    coef[i] = i < j0 ? expf(gt - G_s[i]) * to_f(ut[(size_t)i * kUSub]) : (i == j0 ? un[0] : 0.f);
+                const float eG = expf(gt);
+                float *Srow = const_cast<float *>(S_s) + (size_t)(wt * 32 + row) * kD;
+                __syncthreads();
+                // rotated 16-byte chunks: the lanes (rows) hit distinct bank groups of
+                // the state rows and sweep each key row once; packed FFMA2
+                for (int cc = 0; cc < kD / 4; ++cc) {
+                    const int c4 = 4 * ((cc + lane) & (kD / 4 - 1));
+                    const float4 s4 = *reinterpret_cast<const float4 *>(Srow + c4);
+                    float2 s01 = make_float2(eG * s4.x, eG * s4.y), s23 = make_float2(eG * s4.z, eG * s4.w);
+#pragma unroll
+                    for (int i = 0; i < kFusedFoldMaxC; ++i) {
+                        if (i < J) {
+                            const float4 k4 = *reinterpret_cast<const float4 *>(Kf + i * kD + c4);
+                            const float2 cf = make_float2(coef[i], coef[i]);
+                            s01 = ffma2(cf, make_float2(k4.x, k4.y), s01);
+                            s23 = ffma2(cf, make_float2(k4.z, k4.w), s23);
+                        }
+                    }
+                    *reinterpret_cast<float4 *>(Srow + c4) = make_float4(s01.x, s01.y, s23.x, s23.y);
+                }
+            }
+        }
+    }
+    if constexpr (FOLD) {
+        if (J == dm.C) {   // CTA-uniform: one bulk store of the CTA's folded rows
+            fence_proxy_async_smem();
+            __syncthreads();
+            if (tid == 0) {
+                bulk_s2g(a.p.state + (((size_t)r * Hv + h) * kD + (size_t)tile0 * 32) * kD, S_s, TPC * 32 * kD * 4);
+                bulk_commit();
+            }
+        }
     }
     // ---- 4. records: k_t once per QK head, G_t per V head (first tile group)
     if (tg == 0) {
@@ -639,18 +692,22 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
     if (a.kind != CK_VERIFY && tid == 0 && ticket == (int)(gridDim.x * gridDim.y) - 1) {
         a.p.ticket[r] = 0;
         if (direct) a.p.len[r] = J;
-        else a.p.occ[r] = J;
+        else a.p.occ[r] = (FOLD && J == dm.C) ? 0 : J;
     }
     if (bad) atomicOr(a.p.status, bad);
+    if constexpr (FOLD) {
+        if (J == dm.C && tid == 0) bulk_wait_read0();   // shared memory stays live until the store has read it
+    }
 }
 
 // ---------------------------------------------------------------- launch
-template <typename InT, typename UT, int TPC, int WPT, int NT, bool HAS_STATE, int MBO = 0, bool TC = false>
+template <typename InT, typename UT, int TPC, int WPT, int NT, bool HAS_STATE, int MBO = 0, bool TC = false,
+          bool FOLD = false>
 static cudaError_t launch_cfg(const ChunkArgs &a, cudaStream_t s) {
-    const CtaLayout L = cta_layout(TPC, NT, HAS_STATE, a.j0_cap, sizeof(InT), sizeof(UT), TC);
+    const CtaLayout L = cta_layout(TPC, NT, HAS_STATE, a.j0_cap, sizeof(InT), sizeof(UT), TC, FOLD);
     if (L.bytes > 227 * 1024) return cudaErrorInvalidConfiguration;
     constexpr int MINB = MBO ? MBO : (NT <= 2 ? (HAS_STATE ? 12 / (TPC * WPT) : 2) : 1);
-    auto kfn = chunk_cta_kernel<InT, UT, TPC, WPT, NT, HAS_STATE, MINB < 1 ? 1 : MINB, TC>;
+    auto kfn = chunk_cta_kernel<InT, UT, TPC, WPT, NT, HAS_STATE, MINB < 1 ? 1 : MINB, TC, FOLD>;
     cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.bytes);
     if (e != cudaSuccess) return e;
     CUtensorMap tm;
@@ -676,6 +733,10 @@ static cudaError_t launch_t(const ChunkArgs &a, cudaStream_t s) {
     // 338 -> 281 us at config 4; 5 CTAs spill more and lose); 2 warps per tile
     // for the multi-token kinds was measured slower (195 -> 262-280 us)
     if (a.kind == CK_DIRECT) return launch_nt<InT, UT, kDirectTPC, 1, false, 4>(a, s);
+    if (a.fold) {   // decode with the fused fold (host: some slot fills, C <= 32)
+        if (a.kind != CK_DECODE || a.n_new != 1 || a.dm.C > kFusedFoldMaxC) return cudaErrorInvalidValue;
+        return launch_cfg<InT, UT, kChunkTPC, 1, 1, true, 0, false, true>(a, s);
+    }
     // 8 or more new tokens (verify with N >= 8, prefill chunks): the state
     // mat-vecs on the tensor cores, one CTA per (slot, V head).  Measured at
     // batch 256 (tools/time_verify.py): N = 2 / 4 / 8 -> 197 / 224 / 290 us

@@ -62,6 +62,7 @@ struct ChunkArgs {
     float *o;           // may be null (prefill without outputs)
     int dbg;            // tuning experiments only (LABUF_DEBUG): 1 = skip compute, 2 = skip record copies
     int pdl = 0, pdl_early = 0;   // see Ptrs/launch overlap below
+    int fold = 0;                 // decode: fold a slot's buffer in the step that fills it
     const void *tmap = nullptr;   // host CUtensorMap of the state as [R*Hv*128][128] fp32
                                   // (128 x 32 boxes, 128 B swizzle) for the tensor-core state pass
 };

@@ -58,6 +58,7 @@ struct la_buf {
     std::vector<int32_t> occ, len, mode, pending;   // host mirror
     int64_t launches = 0;
     int overlap = 0;                                 // la_set_overlap
+    int auto_flush = 0;                              // la_set_auto_flush
     alignas(64) unsigned char tmap[128];             // CUtensorMap of the state (tensor-core pass)
     int tmap_state = 0;                              // 0 not built, 1 ok, 2 unavailable
 };
@@ -204,7 +205,7 @@ la_status set_device(la_buf *b) {
 // advanced for decode/direct/prefill, an explicit offset (j_add) for verify.
 cudaError_t run_chunk(la_buf *b, int first, int n, int n_tok, int j0_cap, int tok_base, int tok_total,
                       int kind, const void *q, const void *k, const void *v, const float *alpha,
-                      const float *beta, float *o, cudaStream_t s) {
+                      const float *beta, float *o, cudaStream_t s, int fold = 0) {
     const int mx = max_new_per_launch(b->dm.g);
     const size_t isz = dt_size(b->cfg.in_dtype);
     const size_t d = kD;
@@ -226,9 +227,10 @@ cudaError_t run_chunk(la_buf *b, int first, int n, int n_tok, int j0_cap, int to
             a.o = o ? o + sq * b->dm.Hv * d : nullptr;
             overlap_flags(b, s, a);
             a.tmap = (kind == CK_VERIFY || kind == CK_PREFILL) && m >= 2 ? state_tmap(b) : nullptr;
+            a.fold = fold;
             cudaError_t e = launch_chunk(a, s, &b->launches);
             if (e != cudaSuccess) return e;
-            note_launch(b, s, false);
+            note_launch(b, s, fold != 0);
         }
     }
     return cudaSuccess;
@@ -317,18 +319,24 @@ la_status la_decode_step(la_buf *b, int32_t first, int32_t n, const void *q, con
     if ((st = check_handle(b)) != LA_OK || (st = check_range(b, first, n)) != LA_OK) return st;
     if ((st = check_inputs(q, k, v, alpha, beta, o, true)) != LA_OK) return st;
     int j0_cap = 0;
+    bool fills = false;
     for (int r = first; r < first + n; ++r) {
         if (b->mode[r] != LA_MODE_CHUNKWISE) return fail(LA_ERR_MODE, "slot %d is not CHUNKWISE", r);
         if (b->pending[r]) return fail(LA_ERR_MODE, "slot %d has a pending verify (commit first)", r);
         if (b->occ[r] >= b->cfg.chunk) return fail(LA_ERR_CAPACITY, "slot %d buffer full (call la_flush)", r);
         j0_cap = std::max(j0_cap, b->occ[r]);
+        fills |= b->occ[r] + 1 == b->cfg.chunk;
     }
     if (n == 0) return LA_OK;
     if ((st = set_device(b)) != LA_OK) return st;
+    const int fold = (b->auto_flush && fills && b->cfg.chunk <= 32) ? 1 : 0;
     cudaError_t e = run_chunk(b, first, n, 1, j0_cap, 0, 1, CK_DECODE, q, k, v, alpha, beta, o,
-                              static_cast<cudaStream_t>(stream));
+                              static_cast<cudaStream_t>(stream), fold);
     if (e != cudaSuccess) return cuda_fail(e, "decode launch");
-    for (int r = first; r < first + n; ++r) b->occ[r] += 1;
+    for (int r = first; r < first + n; ++r) {
+        b->occ[r] += 1;
+        if (fold && b->occ[r] == b->cfg.chunk) b->occ[r] = 0;   // folded in the same kernel
+    }
     return LA_OK;
 }
 
@@ -533,6 +541,14 @@ la_status la_recurrent_commit(la_buf *b, int32_t first, int32_t n, int32_t n_dra
     cudaError_t e = launch_recurrent_commit(a, static_cast<cudaStream_t>(stream), &b->launches);
     if (e != cudaSuccess) return cuda_fail(e, "recurrent commit launch");
     note_launch(b, static_cast<cudaStream_t>(stream), true);
+    return LA_OK;
+}
+
+la_status la_set_auto_flush(la_buf *b, int32_t enable) {
+    la_status st;
+    if ((st = check_handle(b)) != LA_OK) return st;
+    if (enable != 0 && enable != 1) return fail(LA_ERR_INVALID, "enable must be 0 or 1");
+    b->auto_flush = enable;
     return LA_OK;
 }
 

@@ -12,7 +12,9 @@ from paper_2605_19049_b200 import labuf as L
 
 B, C, Hk, Hv = 64, 16, 16, 32
 reps = int(sys.argv[1]) if len(sys.argv) > 1 else 1
+fused = len(sys.argv) > 2 and sys.argv[2] == "fused"
 buf = L.LaBuf(L.make_config(B, Hk, Hv, chunk=C), device="cuda")
+buf.set_auto_flush(fused)
 buf.reset(zero_state=False)
 buf.state.copy_(sd.state0(1, B, Hv))
 xs = [sd.tokens(10 + t, B, 1, Hk, Hv, squeeze=True) for t in range(C)]
