@@ -182,3 +182,26 @@ def test_binding_has_no_fallback(tmp_path):
             mod.load_library(str(tmp_path / "missing.so"))
     finally:
         mod._lib = saved
+
+
+def test_launch_options_and_raw_flag_validation(lib):
+    """la_set_overlap / la_set_auto_flush accept 0/1 only; LA_FLUSH_RAW needs
+    a keep_raw handle (rejected before any device work, mirror unchanged);
+    the header and the binding agree on the flag values."""
+    hdr = open(HEADER).read()
+    assert "LA_FLUSH_RAW = 2" in hdr and L.LA_FLUSH_RAW == 2
+    h = _fake_handle(lib, _cfg())
+    for fn in (lib.la_set_overlap, lib.la_set_auto_flush):
+        assert fn(h, 1) == L.LA_OK and fn(h, 0) == L.LA_OK
+        assert fn(h, 2) == L.LA_ERR_INVALID and fn(h, -1) == L.LA_ERR_INVALID
+        assert fn(None, 1) == L.LA_ERR_INVALID
+    assert lib.la_flush(h, 0, 1, L.LA_FLUSH_FORCE | L.LA_FLUSH_RAW, None) == L.LA_ERR_INVALID
+    assert lib.la_flush(h, 0, 1, L.LA_FLUSH_FULL | L.LA_FLUSH_RAW, None) == L.LA_ERR_INVALID
+    assert lib.la_flush(h, 0, 1, 4 | L.LA_FLUSH_FULL, None) == L.LA_ERR_INVALID
+    assert lib.la_kernel_launches(h) == 0
+    lib.la_buf_destroy(h)
+    # with keep_raw the raw flag passes the host checks (empty flush: no-op)
+    h = _fake_handle(lib, _cfg(keep_raw=True))
+    assert lib.la_flush(h, 0, 8, L.LA_FLUSH_FULL | L.LA_FLUSH_RAW, None) == L.LA_OK
+    assert lib.la_kernel_launches(h) == 0
+    lib.la_buf_destroy(h)
