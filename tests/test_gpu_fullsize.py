@@ -61,11 +61,12 @@ def test_config2_full_batch_graph_cycle(cuda_device):
     assert flags == 0 and occ == [0] * B
 
 
-def test_config3_full_batch_verify_commit(cuda_device):
-    """Config 3: batch 256, 4 drafts, parallel verify + accepted-prefix commit
-    with p_accept = 0.7, three rounds after a 3-token decode prefix; sampled
-    slots cover every n_acc value."""
-    B, N, C = 256, 4, 16
+@pytest.mark.parametrize("N", [4, 8])
+def test_config3_full_batch_verify_commit(cuda_device, N):
+    """Config 3: batch 256, 4 drafts (8: the tensor-core state pass), parallel
+    verify + accepted-prefix commit with p_accept = 0.7, three rounds after a
+    3-token decode prefix; sampled slots cover every n_acc value."""
+    B, C = 256, 16
     buf = make_buf(B, HK, HV, C=C, N=N, validate=False)
     buf.reset(zero_state=False)
     S0 = sd.state0(2003, B, HV, device=cuda_device)
