@@ -449,6 +449,33 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
                     if (xid[o] >= 0 && t < n_new) ((xid[o] & 1) ? bv : av)[(wt * NT + t) * 32 + rf] = res[o];
                 }
             }
+        } else if constexpr (HAS_STATE && V <= 8 && WPT == 1) {
+            // 2 or 4 new tokens (verify): lane owns columns 4 lane .. 4 lane + 3 of
+            // all V = 2 NT vectors (k_t, q_t) in registers and reads whole state
+            // rows (one conflict-free 16-byte read per row); RB = 32 / V rows per
+            // batch give 32 partial sums per lane, summed across the warp by one
+            // transposed butterfly (lane l ends with value l = (row l / V, vector l % V))
+            constexpr int RB = 32 / V;
+            float4 vec[V];
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+                if constexpr (KQ32) vec[v] = *reinterpret_cast<const float4 *>(kq32 + (size_t)v * kD + 4 * lane);
+                else vec[v] = load4(((v & 1) ? q_s : k_s) + (size_t)(v >> 1) * kD + 4 * lane);
+            }
+#pragma unroll 1
+            for (int rb = 0; rb < 32; rb += RB) {
+                float vals[32];
+#pragma unroll
+                for (int rr = 0; rr < RB; ++rr) {
+                    const float4 s4 = *reinterpret_cast<const float4 *>(S_s + (size_t)(wt * 32 + rb + rr) * kD + 4 * lane);
+#pragma unroll
+                    for (int v = 0; v < V; ++v)
+                        vals[rr * V + v] = fmaf(s4.x, vec[v].x, fmaf(s4.y, vec[v].y, fmaf(s4.z, vec[v].z, s4.w * vec[v].w)));
+                }
+                const float red = transposed_reduce<32>(vals, lane);
+                const int row = rb + lane / V, v = lane % V, t = v >> 1;
+                if (t < n_new) ((v & 1) ? bv : av)[(wt * NT + t) * 32 + row] = red;
+            }
         } else if constexpr (HAS_STATE) {
             static_assert(RPW % 16 == 0, "two row blocks per step");
             constexpr int NOUT2 = TeamOut<2 * V>::N;
