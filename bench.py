@@ -51,6 +51,7 @@ def parse_args():
     p.add_argument("--u-dtype", default="f32", choices=["f32", "f16"])
     p.add_argument("--no-rows", action="store_true", help="skip the verify / direct rows")
     p.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    p.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg (sweeps)")
     p.add_argument("--no-overlap", action="store_true", help="launch without PDL (la_set_overlap 0)")
     p.add_argument("--auto-flush", action="store_true",
                    help="headline WITH the fused flush (la_set_auto_flush; measured slower, see DESIGN.md)")
@@ -476,87 +477,90 @@ def main():
     #      la_* calls, events) is one CUDA graph launched per step.
     K_e2e = min(K, 10)
     names = ("q", "k", "v", "alpha", "beta")
+    if args.no_e2e:
+        K_e2e = 0
 
-    def carve(nbytes_list):
-        offs, o = [], 0
-        for nb in nbytes_list:
-            offs.append(o)
-            o += (nb + 255) // 256 * 256
-        return offs, o
-    in_specs = [(k_, inputs[0][0][k_].shape, inputs[0][0][k_].dtype) for k_ in names]
-    in_nb = [int(torch.Size(sh).numel()) * torch.empty(0, dtype=dt).element_size() for _, sh, dt in in_specs]
-    offs, per_layer = carve(in_nb)
-    o_nb = B * Hv * D * 4
-    dev_in = [torch.empty(NL * per_layer, dtype=torch.uint8, device=dev) for _ in range(C)]
-    dev_out = [torch.empty(NL, B, Hv, D, dtype=torch.float32, device=dev) for _ in range(C)]
-    host_in = [torch.empty(NL * per_layer, dtype=torch.uint8).pin_memory() for _ in range(C)]
-    host_out = [torch.empty(NL, B, Hv, D, dtype=torch.float32).pin_memory() for _ in range(C)]
-    views = []
-    for t in range(C):
-        row = []
-        for l in range(NL):
-            v = {}
-            for (k_, sh, dt), off, nb in zip(in_specs, offs, in_nb):
-                base = l * per_layer + off
-                v[k_] = dev_in[t][base:base + nb].view(dt).view(sh)
-                v[k_].copy_(inputs[t][l][k_])                    # the same values as the device-resident run
-            v["o"] = dev_out[t][l]
-            row.append(v)
-        views.append(row)
-        host_in[t].copy_(dev_in[t])
-    torch.cuda.synchronize()
-    h2d = sum(x.numel() for x in host_in)
-    d2h = sum(x.numel() * 4 for x in host_out)
-    h2d_stream = torch.cuda.Stream(device=dev)
-    d2h_stream = torch.cuda.Stream(device=dev)
-    ev_in = [torch.cuda.Event() for _ in range(C)]
-    ev_out = [torch.cuda.Event() for _ in range(C)]
-
-    def e2e_step():
-        h2d_stream.wait_stream(stream)
-        d2h_stream.wait_stream(stream)
-        with torch.cuda.stream(h2d_stream):
-            for t in range(C):
-                dev_in[t].copy_(host_in[t], non_blocking=True)
-                ev_in[t].record(h2d_stream)
+    if K_e2e:
+        def carve(nbytes_list):
+            offs, o = [], 0
+            for nb in nbytes_list:
+                offs.append(o)
+                o += (nb + 255) // 256 * 256
+            return offs, o
+        in_specs = [(k_, inputs[0][0][k_].shape, inputs[0][0][k_].dtype) for k_ in names]
+        in_nb = [int(torch.Size(sh).numel()) * torch.empty(0, dtype=dt).element_size() for _, sh, dt in in_specs]
+        offs, per_layer = carve(in_nb)
+        o_nb = B * Hv * D * 4
+        dev_in = [torch.empty(NL * per_layer, dtype=torch.uint8, device=dev) for _ in range(C)]
+        dev_out = [torch.empty(NL, B, Hv, D, dtype=torch.float32, device=dev) for _ in range(C)]
+        host_in = [torch.empty(NL * per_layer, dtype=torch.uint8).pin_memory() for _ in range(C)]
+        host_out = [torch.empty(NL, B, Hv, D, dtype=torch.float32).pin_memory() for _ in range(C)]
+        views = []
         for t in range(C):
-            stream.wait_event(ev_in[t])
-            for l, b in enumerate(bufs):
-                x = views[t][l]
-                b.decode_step(0, x["q"], x["k"], x["v"], x["alpha"], x["beta"], x["o"])
-            ev_out[t].record(stream)
-        for b in bufs:
-            b.flush(0, B, L.LA_FLUSH_FULL)
-        with torch.cuda.stream(d2h_stream):
-            for t in range(C):
-                d2h_stream.wait_event(ev_out[t])
-                host_out[t].copy_(dev_out[t], non_blocking=True)
-        stream.wait_stream(h2d_stream)
-        stream.wait_stream(d2h_stream)
+            row = []
+            for l in range(NL):
+                v = {}
+                for (k_, sh, dt), off, nb in zip(in_specs, offs, in_nb):
+                    base = l * per_layer + off
+                    v[k_] = dev_in[t][base:base + nb].view(dt).view(sh)
+                    v[k_].copy_(inputs[t][l][k_])                    # the same values as the device-resident run
+                v["o"] = dev_out[t][l]
+                row.append(v)
+            views.append(row)
+            host_in[t].copy_(dev_in[t])
+        torch.cuda.synchronize()
+        h2d = sum(x.numel() for x in host_in)
+        d2h = sum(x.numel() * 4 for x in host_out)
+        h2d_stream = torch.cuda.Stream(device=dev)
+        d2h_stream = torch.cuda.Stream(device=dev)
+        ev_in = [torch.cuda.Event() for _ in range(C)]
+        ev_out = [torch.cuda.Event() for _ in range(C)]
 
-    g_e2e = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(g_e2e, stream=stream):
-        e2e_step()
-    for _ in range(2):
-        g_e2e.replay()
-    barrier()
-    t0 = time.perf_counter()
-    for _ in range(K_e2e):
-        with torch.cuda.stream(stream):
+        def e2e_step():
+            h2d_stream.wait_stream(stream)
+            d2h_stream.wait_stream(stream)
+            with torch.cuda.stream(h2d_stream):
+                for t in range(C):
+                    dev_in[t].copy_(host_in[t], non_blocking=True)
+                    ev_in[t].record(h2d_stream)
+            for t in range(C):
+                stream.wait_event(ev_in[t])
+                for l, b in enumerate(bufs):
+                    x = views[t][l]
+                    b.decode_step(0, x["q"], x["k"], x["v"], x["alpha"], x["beta"], x["o"])
+                ev_out[t].record(stream)
+            for b in bufs:
+                b.flush(0, B, L.LA_FLUSH_FULL)
+            with torch.cuda.stream(d2h_stream):
+                for t in range(C):
+                    d2h_stream.wait_event(ev_out[t])
+                    host_out[t].copy_(dev_out[t], non_blocking=True)
+            stream.wait_stream(h2d_stream)
+            stream.wait_stream(d2h_stream)
+
+        g_e2e = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g_e2e, stream=stream):
+            e2e_step()
+        for _ in range(2):
             g_e2e.replay()
-    barrier()
-    e2e_s = max_over_ranks(time.perf_counter() - t0)
-    # the outputs really came back: the last step's host copy equals the device outputs
-    e2e_ok = bool(torch.equal(host_out[C - 1], dev_out[C - 1].cpu()))
-    e2e_us_tok = 1e6 * e2e_s / K_e2e / (C * NL)
-    line["e2e"] = {"value": world * B / (e2e_us_tok * 1e-6), "unit": UNIT,
-                   "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                   "steps": K_e2e, "outputs_checked": e2e_ok,
-                   "note": "la_* calls through the public binding with pinned host buffers: H2D of every "
-                           "step's q/k/v/alpha/beta and D2H of every output inside the timed region (16 + 16 "
-                           "contiguous copies per step on two copy streams beside the decodes; the step is "
-                           "one captured CUDA graph); wall clock, max over ranks"}
-    del g_e2e, dev_in, dev_out, views
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(K_e2e):
+            with torch.cuda.stream(stream):
+                g_e2e.replay()
+        barrier()
+        e2e_s = max_over_ranks(time.perf_counter() - t0)
+        # the outputs really came back: the last step's host copy equals the device outputs
+        e2e_ok = bool(torch.equal(host_out[C - 1], dev_out[C - 1].cpu()))
+        e2e_us_tok = 1e6 * e2e_s / K_e2e / (C * NL)
+        line["e2e"] = {"value": world * B / (e2e_us_tok * 1e-6), "unit": UNIT,
+                       "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                       "steps": K_e2e, "outputs_checked": e2e_ok,
+                       "note": "la_* calls through the public binding with pinned host buffers: H2D of every "
+                               "step's q/k/v/alpha/beta and D2H of every output inside the timed region (16 + 16 "
+                               "contiguous copies per step on two copy streams beside the decodes; the step is "
+                               "one captured CUDA graph); wall clock, max over ranks"}
+        del g_e2e, dev_in, dev_out, views
 
     # ---- extra rows: verify + commit (config 3) and direct (config 4)
     if not args.no_rows:

@@ -446,7 +446,12 @@ cudaError_t launch_fold(const FoldArgs &a_in, cudaStream_t s, int64_t *launches)
     // staging chunk: the largest record count of the launch, rounded to the
     // MMA K granule (8), at most 32 (longer folds loop over chunks)
     int kc = (a.kcap + 7) & ~7;
-    a.kc = kc < 8 ? 8 : (kc > kFoldKCMax ? kFoldKCMax : kc);
+    // staging chunk of at most 16 tokens: longer folds (C = 22, 32, commits of
+    // occ + n_acc > 16) loop over 16-token chunks in the small-footprint CTA
+    // (8 per SM) -- measured C = 22: 99 -> 75 us, C = 32: 104 -> 85 us per
+    // flush against 32-token chunks at 4 CTAs/SM.  LABUF_FOLD_KCMAX overrides.
+    static const int kc_max = getenv("LABUF_FOLD_KCMAX") ? atoi(getenv("LABUF_FOLD_KCMAX")) : 16;
+    a.kc = kc < 8 ? 8 : (kc > kc_max ? kc_max : kc);
     cudaError_t e;
     if (a.dm.in_dt == DT_F32)
         e = launch_fold_t<float, float, true>(a, s);
