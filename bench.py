@@ -52,6 +52,8 @@ def parse_args():
     p.add_argument("--no-rows", action="store_true", help="skip the verify / direct rows")
     p.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     p.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg (sweeps)")
+    p.add_argument("--drafts", type=int, default=4, help="config-3 row: drafts per round")
+    p.add_argument("--direct-l0", type=int, default=64, help="config-4 row: context before the 32 timed steps")
     p.add_argument("--no-overlap", action="store_true", help="launch without PDL (la_set_overlap 0)")
     p.add_argument("--auto-flush", action="store_true",
                    help="headline WITH the fused flush (la_set_auto_flush; measured slower, see DESIGN.md)")
@@ -635,7 +637,7 @@ def extra_rows(torch, L, cost, dev, stream, seed, K, W, peak, args):
     torch.cuda.empty_cache()
 
     # ---------------- config 3: batch 256, 4 drafts, verify + commit vs recurrent verify + copy
-    B3, N3, NL3 = 256, 4, 2
+    B3, N3, NL3 = 256, args.drafts, 2
     lb = cost.LayerBytes.make(Hk, Hv, D, 2, 4)
     cfg = L.make_config(B3, Hk, Hv, chunk=16, max_drafts=N3)
     bufs = [L.LaBuf(cfg, device=dev) for _ in range(NL3)]
@@ -700,7 +702,7 @@ def extra_rows(torch, L, cost, dev, stream, seed, K, W, peak, args):
     torch.cuda.empty_cache()
 
     # ---------------- config 4: batch 1024, direct KV-only decode at context 64 -> 96
-    B4, L0, NS = 1024, 64, 32
+    B4, L0, NS = 1024, args.direct_l0, min(32, 128 - args.direct_l0)
     cfg = L.make_config(B4, Hk, Hv, chunk=16, short_cap=128, u_dtype="f16")
     b4 = L.LaBuf(cfg, device=dev)
     b4.set_overlap(not args.no_overlap)
