@@ -42,7 +42,14 @@
  *   from one host thread at a time.
  * Errors: every function returns la_status.  On any return other than LA_OK
  *   nothing was enqueued and the host occupancy mirror is unchanged
- *   (all-or-nothing); la_last_error() returns a thread-local message.
+ *   (all-or-nothing; every launch configuration of a call is checked before
+ *   the first kernel is enqueued); la_last_error() returns a thread-local
+ *   message.  The one exception is LA_ERR_CUDA from a launch that the driver
+ *   rejects after earlier kernels of the same call were enqueued (e.g. a
+ *   sticky error from an earlier fault): the slots of the call are then in
+ *   an undefined state and must be reset with la_request_reset.
+ * Batches of more than 4096 slots are split into several launches (the slot
+ *   index is a grid dimension).
  * Occupancy: the library keeps an exact host mirror of occ/len/mode per slot;
  *   it advances deterministically (decode +1, flush/commit -> 0, direct +n_new,
  *   prefill -> 0) and never needs device values.  Device copies in `meta`
@@ -218,13 +225,12 @@ LA_API la_status la_recurrent_verify(la_buf *buf, int32_t first, int32_t n, int3
                               float *o, la_stream stream);
 
 /* Baseline commit: the slot's state is replaced by the temporary state of the
- * last accepted draft (Fig. 3); n_accepted = 0 leaves it unchanged. */
+ * last accepted draft (Fig. 3); n_accepted = 0 leaves it unchanged.
+ * Requires CHUNKWISE slots with an empty buffer and no pending verify. */
 LA_API la_status la_recurrent_commit(la_buf *buf, int32_t first, int32_t n, int32_t n_draft,
                               const int32_t *n_accepted, const float *temp,
                               la_stream stream);
 
-/* Canonical state export/import of one slot: fp32 [Hv][d_v][d_k], device
- * pointers, async on `stream`. */
 /* Launch overlap (programmatic dependent launch, B200 griddepcontrol): with
  * enable = 1 every kernel of this handle is launched as a programmatic
  * dependent of the previous kernel on the stream, so its CTAs start while
@@ -251,6 +257,10 @@ LA_API la_status la_set_overlap(la_buf *buf, int32_t enable);
  * LA_ERR_INVALID on enable not 0/1. */
 LA_API la_status la_set_auto_flush(la_buf *buf, int32_t enable);
 
+/* Canonical state export/import of one slot: fp32 [Hv][d_v][d_k], device
+ * pointers, async on `stream`.  la_state_set requires a CHUNKWISE slot with
+ * an empty buffer and no pending verify (the buffered records were computed
+ * against the old state), else LA_ERR_MODE. */
 LA_API la_status la_state_get(la_buf *buf, int32_t slot, float *dst, la_stream stream);
 LA_API la_status la_state_set(la_buf *buf, int32_t slot, const float *src, la_stream stream);
 

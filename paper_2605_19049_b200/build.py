@@ -15,7 +15,6 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "liblabuf.so")
-NCCL_INC = "/opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/nccl/include"
 
 CU_SOURCES = ["chunk.cu", "fold.cu", "recurrent.cu"]
 CPP_SOURCES = ["la.cpp", "tp.cpp"]
@@ -45,7 +44,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     nvcc = os.environ.get("NVCC", "nvcc")
     flags = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
              "-Xcompiler", "-fvisibility=hidden",
-             f"-I{os.path.join(ROOT, 'include')}", f"-I{NCCL_INC}",
+             f"-I{os.path.join(ROOT, 'include')}",
              "-Xptxas", "-warn-spills", "--expt-relaxed-constexpr"]
     if verbose:
         flags.append("-Xptxas=-v")
@@ -54,9 +53,15 @@ def build(force: bool = False, verbose: bool = False) -> str:
     objdir = os.path.join(PKG, "build")
     os.makedirs(objdir, exist_ok=True)
     procs, objs = [], []
+    headers = [p for p in _deps() if not p.endswith((".cu", ".cpp"))]
     for src in _sources():
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
         objs.append(obj)
+        # incremental: an object is rebuilt when it is older than its source
+        # or any shared header (always with force)
+        if not force and os.path.exists(obj) and \
+                os.path.getmtime(obj) >= max(os.path.getmtime(p) for p in [src, *headers]):
+            continue
         procs.append((src, subprocess.Popen([nvcc, *flags, "-c", "-o", obj, src])))
     bad = [src for src, p in procs if p.wait() != 0]
     if bad:

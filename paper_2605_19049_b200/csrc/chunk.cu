@@ -178,6 +178,8 @@ __device__ __forceinline__ float trunc_tf32(float x) { return __uint_as_float(__
 // those rows itself (P:407 on CUDA cores, fp32), and writes S_new: the
 // separate flush, and its second read of the state, disappear.
 constexpr int kFusedFoldMaxC = 32;
+// new tokens from which the state mat-vecs run on the tensor cores
+constexpr int kTcMinTokens = 8;
 
 template <typename InT, typename UT, int TPC, int WPT, int NT, bool HAS_STATE, int MINB, bool TC, bool FOLD = false>
 __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const ChunkArgs a,
@@ -330,22 +332,6 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
         if (lane >= off) x_l += y;
     }
     mbar_wait(full, 0);
-    if (a.dbg & 1) {
-        mbar_wait(recs, 0);
-        if constexpr (TC) {
-            tc_fence_before();
-            __syncthreads();
-            if (warp == 0) tmem_dealloc<32>(*tmem_slot);
-        }
-        if (a.kind != CK_VERIFY && tid == 0 && ticket == (int)(gridDim.x * gridDim.y) - 1) {
-            a.p.ticket[r] = 0;
-            const int Jd = *j0_s + n_new;
-            if (direct) a.p.len[r] = Jd;
-            else a.p.occ[r] = Jd;
-        }
-        return;
-    }
-
     // multi-token launches read k_t / q_t once per row step: widen them to
     // fp32 once per CTA ([t][k | q][128])
     constexpr bool KQ32 = !KQ_REG && isz == 2;
@@ -733,10 +719,12 @@ template <typename InT, typename UT, int TPC, int WPT, int NT, bool HAS_STATE, i
 static cudaError_t launch_cfg(const ChunkArgs &a, cudaStream_t s) {
     const CtaLayout L = cta_layout(TPC, NT, HAS_STATE, a.j0_cap, sizeof(InT), sizeof(UT), TC, FOLD);
     if (L.bytes > 227 * 1024) return cudaErrorInvalidConfiguration;
+    if (a.n > kMaxSlotsPerLaunch) return cudaErrorInvalidConfiguration;
     constexpr int MINB = MBO ? MBO : (NT <= 2 ? (HAS_STATE ? 12 / (TPC * WPT) : 2) : 1);
     auto kfn = chunk_cta_kernel<InT, UT, TPC, WPT, NT, HAS_STATE, MINB < 1 ? 1 : MINB, TC, FOLD>;
     cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.bytes);
     if (e != cudaSuccess) return e;
+    if (a.dry) return cudaSuccess;   // configuration check only (all-or-nothing pre-pass)
     CUtensorMap tm;
     if (TC) tm = *static_cast<const CUtensorMap *>(a.tmap);
     else memset(&tm, 0, sizeof(tm));
@@ -767,17 +755,14 @@ static cudaError_t launch_t(const ChunkArgs &a, cudaStream_t s) {
     // 8 or more new tokens (verify with N >= 8, prefill chunks): the state
     // mat-vecs on the tensor cores, one CTA per (slot, V head).  Measured at
     // batch 256 (tools/time_verify.py): N = 2 / 4 / 8 -> 197 / 224 / 290 us
-    // vs 107 / 189 / 322 us on the CUDA cores.  LABUF_TC=0 forces CUDA cores.
-    static const int tc_env = getenv("LABUF_TC") ? atoi(getenv("LABUF_TC")) : 8;
-    if (tc_env && a.n_new >= tc_env && a.n_new >= 2 && a.tmap) return launch_nt<InT, UT, 4, 1, true, 1, true>(a, s);
+    // vs 107 / 189 / 322 us on the CUDA cores.
+    if (a.n_new >= kTcMinTokens && a.tmap) return launch_nt<InT, UT, 4, 1, true, 1, true>(a, s);
     return launch_nt<InT, UT, kChunkTPC, 1, true>(a, s);
 }
 
 cudaError_t launch_chunk(const ChunkArgs &a_in, cudaStream_t s, int64_t *launches) {
     if (a_in.n <= 0 || a_in.n_new <= 0) return cudaSuccess;
-    static const int dbg = getenv("LABUF_DEBUG") ? atoi(getenv("LABUF_DEBUG")) : 0;
-    ChunkArgs a = a_in;
-    a.dbg = dbg;
+    const ChunkArgs &a = a_in;
     if (a.n_new > max_new_per_launch(a.dm.g)) return cudaErrorInvalidValue;
     cudaError_t e;
     if (a.dm.in_dt == DT_F32)
@@ -786,7 +771,7 @@ cudaError_t launch_chunk(const ChunkArgs &a_in, cudaStream_t s, int64_t *launche
         e = launch_t<__nv_bfloat16, __half>(a, s);
     else
         e = launch_t<__nv_bfloat16, float>(a, s);
-    if (e == cudaSuccess) ++*launches;
+    if (e == cudaSuccess && !a.dry) ++*launches;
     return e;
 }
 

@@ -22,14 +22,12 @@
 // the row-major state tile), adds e^{G_last} S0 in shared memory and one
 // bulk store writes S_new back.  Shared memory is sized from the host-known
 // largest record count, so 4 CTAs share an SM at C = 16.
-#include <cstdlib>
-
 #include "device.cuh"
 #include "internal.h"
 
 namespace labuf {
 
-constexpr int kFoldKCMax = 32;   // tokens per MMA staging chunk (max)
+constexpr int kFoldKCMax = 16;   // tokens per MMA staging chunk (max)
 constexpr int kFoldThreads = 128;
 
 struct FoldSmem {
@@ -422,36 +420,24 @@ static cudaError_t launch_fold_t(const FoldArgs &a, cudaStream_t s) {
     // many CTAs fold little or nothing (commits: zero or few accepted drafts)
     // take 64-row CTAs (half the CTAs): config-3 commit 164 -> 127 us.  Full
     // flushes keep 32-row CTAs (more CTAs per SM in flight): 57 vs 62 us.
-    // LABUF_FOLD_NJ=32/64/128 forces one size (tuning sweeps).
-    static const int nj_env = getenv("LABUF_FOLD_NJ") ? atoi(getenv("LABUF_FOLD_NJ")) : 0;
-    const int nj = nj_env ? nj_env : (a.spec ? 32 : 64);
-    if (a.raw)
-        return a.kc <= 16 ? launch_fold_cfg<InT, UT, FP32_IN, 32, 16, true>(a, s)
-                          : launch_fold_cfg<InT, UT, FP32_IN, 32, 32, true>(a, s);
-    if (nj == 128)
-        return a.kc <= 16 ? launch_fold_cfg<InT, UT, FP32_IN, 128, 16, false>(a, s)
-                          : launch_fold_cfg<InT, UT, FP32_IN, 128, 32, false>(a, s);
-    if (nj == 64)
-        return a.kc <= 16 ? launch_fold_cfg<InT, UT, FP32_IN, 64, 16, false>(a, s)
-                          : launch_fold_cfg<InT, UT, FP32_IN, 64, 32, false>(a, s);
-    return a.kc <= 16 ? launch_fold_cfg<InT, UT, FP32_IN, 32, 16, false>(a, s)
-                      : launch_fold_cfg<InT, UT, FP32_IN, 32, 32, false>(a, s);
+    const int nj = a.spec ? 32 : 64;
+    if (a.raw) return launch_fold_cfg<InT, UT, FP32_IN, 32, kFoldKCMax, true>(a, s);
+    if (nj == 64) return launch_fold_cfg<InT, UT, FP32_IN, 64, kFoldKCMax, false>(a, s);
+    return launch_fold_cfg<InT, UT, FP32_IN, 32, kFoldKCMax, false>(a, s);
 }
 
 cudaError_t launch_fold(const FoldArgs &a_in, cudaStream_t s, int64_t *launches) {
     if (a_in.n <= 0) return cudaSuccess;
     FoldArgs a = a_in;
-    static const int spec_env = getenv("LABUF_FOLD_SPEC") ? atoi(getenv("LABUF_FOLD_SPEC")) : 1;
-    a.spec &= spec_env;
+    if (a.n > kMaxSlotsPerLaunch) return cudaErrorInvalidConfiguration;
     // staging chunk: the largest record count of the launch, rounded to the
     // MMA K granule (8), at most 32 (longer folds loop over chunks)
     int kc = (a.kcap + 7) & ~7;
     // staging chunk of at most 16 tokens: longer folds (C = 22, 32, commits of
     // occ + n_acc > 16) loop over 16-token chunks in the small-footprint CTA
     // (8 per SM) -- measured C = 22: 99 -> 75 us, C = 32: 104 -> 85 us per
-    // flush against 32-token chunks at 4 CTAs/SM.  LABUF_FOLD_KCMAX overrides.
-    static const int kc_max = getenv("LABUF_FOLD_KCMAX") ? atoi(getenv("LABUF_FOLD_KCMAX")) : 16;
-    a.kc = kc < 8 ? 8 : (kc > kc_max ? kc_max : kc);
+    // flush against 32-token chunks at 4 CTAs/SM.
+    a.kc = kc < 8 ? 8 : (kc > kFoldKCMax ? kFoldKCMax : kc);
     cudaError_t e;
     if (a.dm.in_dt == DT_F32)
         e = launch_fold_t<float, float, true>(a, s);

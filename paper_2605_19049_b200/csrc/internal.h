@@ -60,7 +60,7 @@ struct ChunkArgs {
     const void *q, *k, *v;
     const float *alpha, *beta;
     float *o;           // may be null (prefill without outputs)
-    int dbg;            // tuning experiments only (LABUF_DEBUG): 1 = skip compute, 2 = skip record copies
+    int dry = 0;        // 1: check the launch configuration only, enqueue nothing
     int pdl = 0, pdl_early = 0;   // see Ptrs/launch overlap below
     int fold = 0;                 // decode: fold a slot's buffer in the step that fills it
     const void *tmap = nullptr;   // host CUtensorMap of the state as [R*Hv*128][128] fp32

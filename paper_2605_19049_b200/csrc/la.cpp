@@ -13,7 +13,9 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "internal.h"
@@ -100,26 +102,36 @@ const void *state_tmap(la_buf *b) {
     return b->tmap_state == 1 ? b->tmap : nullptr;
 }
 
-// The library's last kernel launch on this host thread: whose state it was,
-// on which stream, and whether it wrote that state.  A launch with overlap
-// requests its state tiles before griddepcontrol.wait only if the kernel it
-// overlaps (the previous one on the stream) cannot have written them.
+// Launch overlap bookkeeping.  With programmatic dependent launch a kernel's
+// CTAs may start while the kernel immediately before it on the same stream
+// drains; every kernel of the library calls griddepcontrol.launch_dependents
+// only after its own griddepcontrol.wait, so no older kernel can still be
+// running.  A kernel may therefore request its state tiles before the wait
+// only if that immediate predecessor did not write the same state.  The
+// record is kept per STREAM (process-wide), for the library's own launches:
+// the last launch on the stream, whose state it was and whether it wrote it.
+// g_enqueue_mu is held from the decision through the launch and the record,
+// so concurrent callers on one stream (different handles, different threads)
+// see the records in stream order.
 struct LastLaunch {
     const void *state = nullptr;
-    cudaStream_t s = nullptr;
     bool wrote = false;
 };
-thread_local LastLaunch g_last;
+std::mutex g_enqueue_mu;
+std::unordered_map<cudaStream_t, LastLaunch> g_last_on_stream;
 
 template <class Args>
 void overlap_flags(const la_buf *b, cudaStream_t s, Args &a) {
     a.pdl = b->overlap;
-    a.pdl_early = b->overlap && !(g_last.s == s && g_last.wrote && g_last.state == b->p.state);
+    bool prev_wrote_mine = false;
+    auto it = g_last_on_stream.find(s);
+    if (it != g_last_on_stream.end()) prev_wrote_mine = it->second.wrote && it->second.state == b->p.state;
+    a.pdl_early = b->overlap && !prev_wrote_mine;
 }
 void note_launch(const la_buf *b, cudaStream_t s, bool wrote_state) {
-    g_last.state = b->p.state;
-    g_last.s = s;
-    g_last.wrote = wrote_state;
+    LastLaunch &l = g_last_on_stream[s];
+    l.state = b->p.state;
+    l.wrote = wrote_state;
 }
 
 la_status check_config(const la_config *c) {
@@ -209,29 +221,82 @@ cudaError_t run_chunk(la_buf *b, int first, int n, int n_tok, int j0_cap, int to
     const int mx = max_new_per_launch(b->dm.g);
     const size_t isz = dt_size(b->cfg.in_dtype);
     const size_t d = kD;
-    for (int off = 0; off < n_tok; off += mx) {
-        const int m = std::min(mx, n_tok - off);
-        for (int s0 = 0; s0 < n; s0 += kMaxSlotsPerLaunch) {
-            ChunkArgs a;
-            a.dm = b->dm; a.p = b->p;
-            a.first = first + s0; a.n = std::min(kMaxSlotsPerLaunch, n - s0);
-            a.n_new = m; a.j0_cap = j0_cap + off;
-            a.j_add = (kind == CK_VERIFY) ? off : 0;
-            a.tok_total = tok_total; a.tok_offset = tok_base + off; a.kind = kind;
-            const size_t sq = (size_t)s0 * tok_total;          // token rows skipped
-            a.q = static_cast<const char *>(q) + sq * b->dm.Hk * d * isz;
-            a.k = static_cast<const char *>(k) + sq * b->dm.Hk * d * isz;
-            a.v = static_cast<const char *>(v) + sq * b->dm.Hv * d * isz;
-            a.alpha = alpha + sq * b->dm.Hv;
-            a.beta = beta + sq * b->dm.Hv;
-            a.o = o ? o + sq * b->dm.Hv * d : nullptr;
-            overlap_flags(b, s, a);
-            a.tmap = (kind == CK_VERIFY || kind == CK_PREFILL) && m >= 2 ? state_tmap(b) : nullptr;
-            a.fold = fold;
-            cudaError_t e = launch_chunk(a, s, &b->launches);
-            if (e != cudaSuccess) return e;
-            note_launch(b, s, fold != 0);
+    // pass 0 checks every launch configuration (shared memory, grid) without
+    // enqueueing anything, so a configuration error leaves the handle and the
+    // device untouched (all-or-nothing); pass 1 enqueues
+    for (int pass = 0; pass < 2; ++pass) {
+        for (int off = 0; off < n_tok; off += mx) {
+            const int m = std::min(mx, n_tok - off);
+            for (int s0 = 0; s0 < n; s0 += kMaxSlotsPerLaunch) {
+                ChunkArgs a;
+                a.dm = b->dm; a.p = b->p;
+                a.first = first + s0; a.n = std::min(kMaxSlotsPerLaunch, n - s0);
+                a.n_new = m; a.j0_cap = j0_cap + off;
+                a.j_add = (kind == CK_VERIFY) ? off : 0;
+                a.tok_total = tok_total; a.tok_offset = tok_base + off; a.kind = kind;
+                const size_t sq = (size_t)s0 * tok_total;          // token rows skipped
+                a.q = static_cast<const char *>(q) + sq * b->dm.Hk * d * isz;
+                a.k = static_cast<const char *>(k) + sq * b->dm.Hk * d * isz;
+                a.v = static_cast<const char *>(v) + sq * b->dm.Hv * d * isz;
+                a.alpha = alpha + sq * b->dm.Hv;
+                a.beta = beta + sq * b->dm.Hv;
+                a.o = o ? o + sq * b->dm.Hv * d : nullptr;
+                a.tmap = (kind == CK_VERIFY || kind == CK_PREFILL) && m >= 2 ? state_tmap(b) : nullptr;
+                a.fold = fold;
+                a.dry = pass == 0;
+                overlap_flags(b, s, a);
+                cudaError_t e = launch_chunk(a, s, &b->launches);
+                if (e != cudaSuccess) return e;
+                if (pass == 1) note_launch(b, s, fold != 0);
+            }
         }
+    }
+    return cudaSuccess;
+}
+
+// Folds (flush, commit, compression) in slot batches of kMaxSlotsPerLaunch
+// (the slot index is a grid dimension).
+cudaError_t run_fold(la_buf *b, FoldArgs a, cudaStream_t s) {
+    const int first = a.first, n = a.n;
+    const int *nacc = a.nacc;
+    for (int s0 = 0; s0 < n; s0 += kMaxSlotsPerLaunch) {
+        a.first = first + s0;
+        a.n = std::min(kMaxSlotsPerLaunch, n - s0);
+        a.nacc = nacc ? nacc + s0 : nullptr;
+        overlap_flags(b, s, a);
+        cudaError_t e = launch_fold(a, s, &b->launches);
+        if (e != cudaSuccess) return e;
+        note_launch(b, s, true);
+    }
+    return cudaSuccess;
+}
+
+// Recurrent kernels (5a)/(5b)/commit in slot batches; per-slot arrays
+// (inputs [n][n_draft][...], outputs, temporary states, n_accepted) advance
+// with the batch.
+template <class Launch>
+cudaError_t run_rec(la_buf *b, RecArgs a, cudaStream_t s, bool wrote, Launch launch) {
+    const int first = a.first, n = a.n, N = a.n_draft;
+    const size_t isz = dt_size(b->cfg.in_dtype), d = kD, Hk = b->dm.Hk, Hv = b->dm.Hv;
+    const RecArgs a0 = a;
+    for (int s0 = 0; s0 < n; s0 += kMaxSlotsPerLaunch) {
+        const size_t sq = (size_t)s0 * N;
+        a.first = first + s0;
+        a.n = std::min(kMaxSlotsPerLaunch, n - s0);
+        if (a0.q) {
+            a.q = static_cast<const char *>(a0.q) + sq * Hk * d * isz;
+            a.k = static_cast<const char *>(a0.k) + sq * Hk * d * isz;
+            a.v = static_cast<const char *>(a0.v) + sq * Hv * d * isz;
+            a.alpha = a0.alpha + sq * Hv;
+            a.beta = a0.beta + sq * Hv;
+            a.o = a0.o + sq * Hv * d;
+        }
+        if (a0.temp) a.temp = a0.temp + sq * Hv * d * d;
+        if (a0.nacc) a.nacc = a0.nacc + s0;
+        overlap_flags(b, s, a);
+        cudaError_t e = launch(a, s, &b->launches);
+        if (e != cudaSuccess) return e;
+        note_launch(b, s, wrote);
     }
     return cudaSuccess;
 }
@@ -297,13 +362,16 @@ la_status la_request_reset(la_buf *b, int32_t first, int32_t n, int32_t mode, in
     if (mode == LA_MODE_DIRECT && b->cfg.short_cap == 0) return fail(LA_ERR_MODE, "direct mode disabled (short_cap = 0)");
     if (n == 0) return LA_OK;
     if ((st = set_device(b)) != LA_OK) return st;
-    cudaError_t e = launch_reset(b->dm, b->p, first, n, mode, zero_state ? 1 : 0,
-                                 static_cast<cudaStream_t>(stream), &b->launches);
-    if (e != cudaSuccess) return cuda_fail(e, "reset launch");
-    note_launch(b, static_cast<cudaStream_t>(stream), zero_state != 0);
+    std::lock_guard<std::mutex> lk(g_enqueue_mu);
+    for (int s0 = 0; s0 < n; s0 += kMaxSlotsPerLaunch) {
+        cudaError_t e = launch_reset(b->dm, b->p, first + s0, std::min(kMaxSlotsPerLaunch, n - s0), mode,
+                                     zero_state ? 1 : 0, static_cast<cudaStream_t>(stream), &b->launches);
+        if (e != cudaSuccess) return cuda_fail(e, "reset launch");
+        note_launch(b, static_cast<cudaStream_t>(stream), zero_state != 0);
+    }
     // status word: cleared by a reset covering slot 0
     if (first == 0) {
-        e = cudaMemsetAsync(b->p.status, 0, sizeof(unsigned), static_cast<cudaStream_t>(stream));
+        cudaError_t e = cudaMemsetAsync(b->p.status, 0, sizeof(unsigned), static_cast<cudaStream_t>(stream));
         if (e != cudaSuccess) return cuda_fail(e, "status clear");
     }
     for (int r = first; r < first + n; ++r) {
@@ -330,6 +398,7 @@ la_status la_decode_step(la_buf *b, int32_t first, int32_t n, const void *q, con
     if (n == 0) return LA_OK;
     if ((st = set_device(b)) != LA_OK) return st;
     const int fold = (b->auto_flush && fills && b->cfg.chunk <= 32) ? 1 : 0;
+    std::lock_guard<std::mutex> lk(g_enqueue_mu);
     cudaError_t e = run_chunk(b, first, n, 1, j0_cap, 0, 1, CK_DECODE, q, k, v, alpha, beta, o,
                               static_cast<cudaStream_t>(stream), fold);
     if (e != cudaSuccess) return cuda_fail(e, "decode launch");
@@ -366,10 +435,9 @@ la_status la_flush(la_buf *b, int32_t first, int32_t n, int32_t kind, la_stream 
     a.dm = b->dm; a.p = b->p; a.first = first; a.n = n;
     a.kind = kind == LA_FLUSH_FULL ? FK_FULL : FK_FORCE; a.nacc = nullptr; a.n_draft = 0; a.kcap = kcap; a.spec = all;
     a.raw = raw ? 1 : 0;
-    overlap_flags(b, static_cast<cudaStream_t>(stream), a);
-    cudaError_t e = launch_fold(a, static_cast<cudaStream_t>(stream), &b->launches);
+    std::lock_guard<std::mutex> lk(g_enqueue_mu);
+    cudaError_t e = run_fold(b, a, static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(e, "flush launch");
-    note_launch(b, static_cast<cudaStream_t>(stream), true);
     for (int r = first; r < first + n; ++r) {
         if (kind == LA_FLUSH_FULL) {
             if (b->mode[r] == LA_MODE_CHUNKWISE && b->occ[r] == b->cfg.chunk) b->occ[r] = 0;
@@ -399,6 +467,7 @@ la_status la_verify_drafts(la_buf *b, int32_t first, int32_t n, int32_t n_draft,
     }
     if (n == 0) return LA_OK;
     if ((st = set_device(b)) != LA_OK) return st;
+    std::lock_guard<std::mutex> lk(g_enqueue_mu);
     cudaError_t e = run_chunk(b, first, n, n_draft, j0_cap, 0, n_draft, CK_VERIFY, q, k, v, alpha, beta, o,
                               static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(e, "verify launch");
@@ -422,10 +491,9 @@ la_status la_commit_accepted(la_buf *b, int32_t first, int32_t n, const int32_t 
     int occ_max = 0;
     for (int r = first; r < first + n; ++r) occ_max = std::max(occ_max, b->occ[r]);
     a.kind = FK_COMMIT; a.nacc = n_accepted; a.n_draft = nd; a.kcap = occ_max + nd; a.spec = 0;
-    overlap_flags(b, static_cast<cudaStream_t>(stream), a);
-    cudaError_t e = launch_fold(a, static_cast<cudaStream_t>(stream), &b->launches);
+    std::lock_guard<std::mutex> lk(g_enqueue_mu);
+    cudaError_t e = run_fold(b, a, static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(e, "commit launch");
-    note_launch(b, static_cast<cudaStream_t>(stream), true);
     for (int r = first; r < first + n; ++r) { b->occ[r] = 0; b->pending[r] = 0; }
     return LA_OK;
 }
@@ -445,6 +513,7 @@ la_status la_direct_short(la_buf *b, int32_t first, int32_t n, int32_t n_new, co
     }
     if (n == 0) return LA_OK;
     if ((st = set_device(b)) != LA_OK) return st;
+    std::lock_guard<std::mutex> lk(g_enqueue_mu);
     cudaError_t e = run_chunk(b, first, n, n_new, j0_cap, 0, n_new, CK_DIRECT, q, k, v, alpha, beta, o,
                               static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(e, "direct launch");
@@ -467,17 +536,16 @@ la_status la_prefill(la_buf *b, int32_t first, int32_t n, int32_t n_tok, const v
     if ((st = set_device(b)) != LA_OK) return st;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const int C = b->cfg.chunk;
+    std::lock_guard<std::mutex> lk(g_enqueue_mu);
     for (int c0 = 0; c0 < n_tok; c0 += C) {
         const int cn = std::min(C, n_tok - c0);
         cudaError_t e = run_chunk(b, first, n, cn, 0, c0, n_tok, CK_PREFILL, q, k, v, alpha, beta, o, s);
-        if (e != cudaSuccess) return cuda_fail(e, "prefill chunk launch");
+        if (e != cudaSuccess) return cuda_fail(e, "prefill chunk launch (the handle's slots are undefined: reset them)");
         FoldArgs f;
         f.dm = b->dm; f.p = b->p; f.first = first; f.n = n; f.kind = FK_FORCE; f.nacc = nullptr; f.n_draft = 0;
         f.kcap = cn; f.spec = 1;
-        overlap_flags(b, s, f);
-        e = launch_fold(f, s, &b->launches);
-        if (e != cudaSuccess) return cuda_fail(e, "prefill fold launch");
-        note_launch(b, s, true);
+        e = run_fold(b, f, s);
+        if (e != cudaSuccess) return cuda_fail(e, "prefill fold launch (the handle's slots are undefined: reset them)");
     }
     return LA_OK;
 }
@@ -496,10 +564,9 @@ la_status la_recurrent_step(la_buf *b, int32_t first, int32_t n, const void *q, 
     RecArgs a{};
     a.dm = b->dm; a.p = b->p; a.first = first; a.n = n; a.n_draft = 1;
     a.q = q; a.k = k; a.v = v; a.alpha = alpha; a.beta = beta; a.o = o;
-    overlap_flags(b, static_cast<cudaStream_t>(stream), a);
-    cudaError_t e = launch_recurrent_step(a, static_cast<cudaStream_t>(stream), &b->launches);
+    std::lock_guard<std::mutex> lk(g_enqueue_mu);
+    cudaError_t e = run_rec(b, a, static_cast<cudaStream_t>(stream), true, launch_recurrent_step);
     if (e != cudaSuccess) return cuda_fail(e, "recurrent step launch");
-    note_launch(b, static_cast<cudaStream_t>(stream), true);
     return LA_OK;
 }
 
@@ -519,10 +586,9 @@ la_status la_recurrent_verify(la_buf *b, int32_t first, int32_t n, int32_t n_dra
     RecArgs a{};
     a.dm = b->dm; a.p = b->p; a.first = first; a.n = n; a.n_draft = n_draft;
     a.q = q; a.k = k; a.v = v; a.alpha = alpha; a.beta = beta; a.o = o; a.temp = temp;
-    overlap_flags(b, static_cast<cudaStream_t>(stream), a);
-    cudaError_t e = launch_recurrent_verify(a, static_cast<cudaStream_t>(stream), &b->launches);
+    std::lock_guard<std::mutex> lk(g_enqueue_mu);
+    cudaError_t e = run_rec(b, a, static_cast<cudaStream_t>(stream), false, launch_recurrent_verify);
     if (e != cudaSuccess) return cuda_fail(e, "recurrent verify launch");
-    note_launch(b, static_cast<cudaStream_t>(stream), false);
     return LA_OK;
 }
 
@@ -532,15 +598,17 @@ la_status la_recurrent_commit(la_buf *b, int32_t first, int32_t n, int32_t n_dra
     if ((st = check_handle(b)) != LA_OK || (st = check_range(b, first, n)) != LA_OK) return st;
     if (!n_accepted || !temp || !aligned(temp, 16)) return fail(LA_ERR_INVALID, "null/misaligned pointer");
     if (n_draft < 1 || n_draft > kMaxNewPerLaunch) return fail(LA_ERR_INVALID, "n_draft outside [1, 16]");
+    for (int r = first; r < first + n; ++r)
+        if (b->mode[r] != LA_MODE_CHUNKWISE || b->occ[r] != 0 || b->pending[r])
+            return fail(LA_ERR_MODE, "slot %d: recurrent commit needs a CHUNKWISE slot with an empty buffer", r);
     if (n == 0) return LA_OK;
     if ((st = set_device(b)) != LA_OK) return st;
     RecArgs a{};
     a.dm = b->dm; a.p = b->p; a.first = first; a.n = n; a.n_draft = n_draft;
     a.nacc = n_accepted; a.temp = const_cast<float *>(temp);
-    overlap_flags(b, static_cast<cudaStream_t>(stream), a);
-    cudaError_t e = launch_recurrent_commit(a, static_cast<cudaStream_t>(stream), &b->launches);
+    std::lock_guard<std::mutex> lk(g_enqueue_mu);
+    cudaError_t e = run_rec(b, a, static_cast<cudaStream_t>(stream), true, launch_recurrent_commit);
     if (e != cudaSuccess) return cuda_fail(e, "recurrent commit launch");
-    note_launch(b, static_cast<cudaStream_t>(stream), true);
     return LA_OK;
 }
 
@@ -576,7 +644,10 @@ la_status la_state_set(la_buf *b, int32_t slot, const float *src, la_stream stre
     la_status st;
     if ((st = check_handle(b)) != LA_OK || (st = check_range(b, slot, 1)) != LA_OK) return st;
     if (!src) return fail(LA_ERR_INVALID, "null src");
+    if (b->mode[slot] != LA_MODE_CHUNKWISE || b->occ[slot] != 0 || b->pending[slot])
+        return fail(LA_ERR_MODE, "slot %d: state_set needs a CHUNKWISE slot with an empty buffer", slot);
     if ((st = set_device(b)) != LA_OK) return st;
+    std::lock_guard<std::mutex> lk(g_enqueue_mu);
     const size_t bytes = (size_t)b->dm.Hv * kD * kD * 4;
     cudaError_t e = cudaMemcpyAsync(b->p.state + (size_t)slot * b->dm.Hv * kD * kD, src, bytes,
                                     cudaMemcpyDeviceToDevice, static_cast<cudaStream_t>(stream));

@@ -4,14 +4,18 @@
 // gathered with one ncclAllGather into a head-major [G][n][Hv/G][d_v] buffer.
 // The data-parallel mode (requests partitioned over GPUs) uses no collective
 // at all.  NCCL is resolved at run time with dlopen so the library has no
-// link-time NCCL dependency (torch's own libnccl.so.2 is reused when loaded).
+// link-time NCCL dependency (torch's own libnccl.so.2 is reused when loaded)
+// and no build-time one either: the few NCCL ABI types used are declared
+// here (they are part of NCCL's stable C ABI), so the library builds where
+// no nccl.h is installed.  LABUF_NCCL_LIB names the shared object to load
+// when libnccl.so.2 is not on the loader path.
 #include "../../include/la.h"
 
 #include <cuda_runtime.h>
 #include <dlfcn.h>
-#include <nccl.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -19,6 +23,15 @@
 extern "C" const char *la_last_error(void);
 
 namespace {
+
+// NCCL C ABI (nccl.h): result codes, the 128-byte unique id, the opaque
+// communicator handle and the uint8 data type tag
+typedef int ncclResult_t;
+constexpr ncclResult_t ncclSuccess = 0;
+typedef struct { char internal[128]; } ncclUniqueId;
+typedef struct ncclComm *ncclComm_t;
+typedef int ncclDataType_t;
+constexpr ncclDataType_t ncclUint8 = 1;
 
 struct NcclApi {
     ncclResult_t (*GetUniqueId)(ncclUniqueId *);
@@ -34,10 +47,10 @@ std::once_flag g_once;
 std::string g_load_error;
 
 void load_nccl() {
-    const char *candidates[] = {
-        "libnccl.so.2",
-        "/opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/nccl/lib/libnccl.so.2",
-    };
+    // an already loaded libnccl.so.2 (torch imports its bundled copy) is
+    // found by soname first
+    const char *env = getenv("LABUF_NCCL_LIB");
+    const char *candidates[] = {env ? env : "libnccl.so.2", "libnccl.so.2", "libnccl.so"};
     void *h = nullptr;
     for (const char *c : candidates) {
         h = dlopen(c, RTLD_NOW | RTLD_GLOBAL);

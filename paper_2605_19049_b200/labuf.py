@@ -69,6 +69,15 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     if not os.path.exists(path):
         raise RuntimeError(f"{path} not found: run `python -m paper_2605_19049_b200.build` "
                            "(the CUDA library is required; there is no fallback)")
+    if "LABUF_NCCL_LIB" not in os.environ:
+        # the tensor-parallel helpers dlopen NCCL; point them at the wheel's copy
+        try:
+            import nvidia.nccl as _nccl
+            cand = os.path.join(list(_nccl.__path__)[0], "lib", "libnccl.so.2")
+            if os.path.exists(cand):
+                os.environ["LABUF_NCCL_LIB"] = cand
+        except Exception:
+            pass
     lib = ctypes.CDLL(path)
     P, I32, VP = ctypes.POINTER, ctypes.c_int32, ctypes.c_void_p
     FP = P(ctypes.c_float)

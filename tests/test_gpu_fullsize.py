@@ -27,9 +27,9 @@ def _capture(fn, stream):
 def test_config2_full_batch_graph_cycle(cuda_device):
     """Config 2: Qwen3-Next GDN layer, batch 64, C = 16, synthetic 32K-context
     states; one captured cycle (16 decode steps + FULL flush) replayed twice,
-    every output and the post-flush states of 5 sampled slots vs the oracle."""
+    every output and the post-flush state of ALL 64 slots vs the oracle."""
     B, C = 64, 16
-    sample = [0, 1, 31, 47, 63]
+    sample = list(range(B))
     buf = make_buf(B, HK, HV, C=C, validate=False)
     buf.reset(zero_state=False)
     S0 = sd.state0(2002, B, HV, device=cuda_device)
