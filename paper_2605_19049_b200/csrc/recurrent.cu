@@ -109,82 +109,116 @@ __global__ void __launch_bounds__(256) recurrent_step_kernel(const RecArgs a) {
 
 // ------------------------------------------------------------------ (5b)
 // N sequential recurrent steps from one state read; writes N temporary
-// states [n][N][Hv][d][d] and N outputs.  Rows stay in
-// registers across steps; each warp owns RPW rows.
-template <typename InT, int G>
-__global__ void __launch_bounds__(256) recurrent_verify_kernel(const RecArgs a) {
-    constexpr int ROWS = kRows, GR = G * ROWS, RPW = GR / 8;
-    constexpr int NV = 2 * RPW;          // RPW <= 16 -> NV <= 32
-    const int tile = blockIdx.x, hk = blockIdx.y, zi = blockIdx.z;
+// states [n][N][Hv][d][d] and N outputs.  CTA = (d_v tile of
+// kRows rows, V head, slot), 4 warps x 8 rows; the rows stay in registers
+// across the drafts.  Every operand is staged at entry (state tile by one
+// bulk copy; k_t, q_t, v_t of all drafts by bulk copies; alpha, beta) so the
+// draft loop has no global loads, and each temporary state leaves through a
+// double-buffered shared-memory tile and ONE bulk store (the TMA engine, not
+// per-lane stores, drains the N x 16 KiB of writes per CTA) -- the same
+// machinery as kernel (5a), so the baseline streams at the copy roofline.
+template <typename InT>
+__global__ void __launch_bounds__(128) recurrent_verify_kernel(const RecArgs a) {
+    constexpr int ROWS = kRows, RPW = ROWS / 4, isz = (int)sizeof(InT);
+    static_assert(RPW == 8, "4 warps x 8 rows");
+    const int tile = blockIdx.x, h = blockIdx.y, zi = blockIdx.z;
     const int r = a.first + zi;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int Hv = a.dm.Hv, Hk = a.dm.Hk, N = a.n_draft;
+    const int Hv = a.dm.Hv, Hk = a.dm.Hk, N = a.n_draft, hk = h / a.dm.g;
 
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t *bar = reinterpret_cast<uint64_t *>(smem);
-    float *S_s = reinterpret_cast<float *>(smem + 128);
-    float *ab = S_s + GR * kD;           // [8 warps][NV]
+    float *buf = reinterpret_cast<float *>(smem + 128);             // [2][ROWS][kD]
+    InT *kq_s = reinterpret_cast<InT *>(buf + 2 * ROWS * kD);        // [N][k | q][kD]
+    InT *v_s = kq_s + (size_t)N * 2 * kD;                            // [N][ROWS]
+    float *al_s = reinterpret_cast<float *>(v_s + (size_t)N * ROWS); // [N]
+    float *be_s = al_s + 16;
+    float *kqd = be_s + 16;                                          // k_t . q_t
 
-    auto load_state = [&]() {
-#pragma unroll
-        for (int hh = 0; hh < G; ++hh)
-            bulk_g2s(S_s + hh * ROWS * kD,
-                     a.p.state + (((size_t)r * Hv + hk * G + hh) * kD + (size_t)tile * ROWS) * kD,
-                     ROWS * kD * 4, bar);
-    };
+    const float *src = a.p.state + (((size_t)r * Hv + h) * kD + (size_t)tile * ROWS) * kD;
+    const uint32_t bytes = ROWS * kD * 4 + (uint32_t)N * (2 * kD + ROWS) * isz;
     if (tid == 0) {
         mbar_init(bar, 1);
         fence_mbar_init();
-        mbar_arrive_expect_tx(bar, GR * kD * 4);
-        if (a.pdl_early) load_state();
+        if (a.pdl_early) {
+            mbar_arrive_expect_tx(bar, bytes);
+            bulk_g2s(buf, src, ROWS * kD * 4, bar);
+        }
     }
     if (a.pdl) pdl_wait();
     pdl_trigger();
-    if (tid == 0 && !a.pdl_early) load_state();
-    __syncthreads();
-    mbar_wait(bar, 0);
-    float4 s[RPW];
-#pragma unroll
-    for (int rr = 0; rr < RPW; ++rr)
-        s[rr] = reinterpret_cast<const float4 *>(S_s + (size_t)(warp * RPW + rr) * kD)[lane];
+    __syncthreads();   // barrier initialised
     const InT *qin = static_cast<const InT *>(a.q);
     const InT *kin = static_cast<const InT *>(a.k);
     const InT *vin = static_cast<const InT *>(a.v);
-    float *mine = ab + warp * 32;
+    if (tid == 0) {
+        if (!a.pdl_early) {
+            mbar_arrive_expect_tx(bar, bytes);
+            bulk_g2s(buf, src, ROWS * kD * 4, bar);
+        }
+    } else if (warp == 1) {
+        for (int c = lane; c < 3 * N; c += 32) {
+            const int t = c % N, kind = c / N;
+            const size_t tok = (size_t)zi * N + t;
+            if (kind < 2)
+                bulk_g2s(kq_s + ((size_t)t * 2 + kind) * kD, (kind ? qin : kin) + (tok * Hk + hk) * kD, kD * isz, bar);
+            else
+                bulk_g2s(v_s + (size_t)t * ROWS, vin + (tok * Hv + h) * kD + tile * ROWS, ROWS * isz, bar);
+        }
+    } else if (warp == 2 && lane < N) {
+        const size_t tok = (size_t)zi * N + lane;
+        al_s[lane] = a.alpha[tok * Hv + h];
+        be_s[lane] = a.beta[tok * Hv + h];
+    }
+    mbar_wait(bar, 0);
+    for (int t = warp; t < N; t += 4) {
+        const float x = warp_sum(dot4(load4(kq_s + (size_t)t * 2 * kD + 4 * lane), load4(kq_s + ((size_t)t * 2 + 1) * kD + 4 * lane)));
+        if (lane == 0) kqd[t] = x;
+    }
+    float4 s[RPW];
+#pragma unroll
+    for (int rr = 0; rr < RPW; ++rr) s[rr] = reinterpret_cast<const float4 *>(buf + (size_t)(warp * RPW + rr) * kD)[lane];
+    __syncthreads();   // kqd visible; every warp holds its rows
+    const int rl = (lane & 15) >> 1;              // the row whose (k | q) dot this lane ends with
+    const int drow = tile * ROWS + warp * RPW + rl;
     for (int t = 0; t < N; ++t) {
-        const size_t tok = (size_t)zi * N + t;
-        const float4 k4 = load4(kin + (tok * Hk + hk) * kD + 4 * lane);
-        const float4 q4 = load4(qin + (tok * Hk + hk) * kD + 4 * lane);
-        const float kq = warp_sum(dot4(k4, q4));
-        float vals[NV];
+        const float4 k4 = load4(kq_s + (size_t)t * 2 * kD + 4 * lane);
+        const float4 q4 = load4(kq_s + ((size_t)t * 2 + 1) * kD + 4 * lane);
+        float vals[2 * RPW];
 #pragma unroll
         for (int rr = 0; rr < RPW; ++rr) {
             vals[2 * rr] = dot4(s[rr], k4);
             vals[2 * rr + 1] = dot4(s[rr], q4);
         }
-        const float red = transposed_reduce<NV>(vals, lane);
-        if (lane < NV) mine[lane] = red;
-        __syncwarp();
+        const float red = transposed_reduce<2 * RPW>(vals, lane);   // lane l: (row (l%16)/2, k|q = l&1)
+        const float al = al_s[t], be = be_s[t];
+        const float uk = be * (to_f(v_s[t * ROWS + warp * RPW + rl]) - al * red);   // valid on even lanes
+        const float u = __shfl_sync(0xffffffffu, uk, lane & ~1);
+        if (lane < 16 && (lane & 1)) {
+            const size_t tok = (size_t)zi * N + t;
+            a.o[(tok * Hv + h) * kD + drow] = fmaf(al, red, u * kqd[t]);
+        }
+        float *dst = buf + (size_t)(t & 1) * ROWS * kD;
 #pragma unroll
         for (int rr = 0; rr < RPW; ++rr) {
-            const int rf = warp * RPW + rr;
-            const int hh = rf / ROWS, row = rf % ROWS, h = hk * G + hh;
-            const int drow = tile * ROWS + row;
-            const float al = a.alpha[tok * Hv + h], be = a.beta[tok * Hv + h];
-            const float vt = to_f(vin[(tok * Hv + h) * kD + drow]);
-            const float u = be * (vt - al * mine[2 * rr]);
-            if (lane == 0) a.o[(tok * Hv + h) * kD + drow] = fmaf(al, mine[2 * rr + 1], u * kq);
+            const float ur = __shfl_sync(0xffffffffu, u, 2 * rr);
             float4 x = s[rr];
-            x.x = fmaf(u, k4.x, al * x.x);
-            x.y = fmaf(u, k4.y, al * x.y);
-            x.z = fmaf(u, k4.z, al * x.z);
-            x.w = fmaf(u, k4.w, al * x.w);
+            x.x = fmaf(ur, k4.x, al * x.x);
+            x.y = fmaf(ur, k4.y, al * x.y);
+            x.z = fmaf(ur, k4.z, al * x.z);
+            x.w = fmaf(ur, k4.w, al * x.w);
             s[rr] = x;
-            float *dst = a.temp + ((((size_t)zi * N + t) * Hv + h) * kD + drow) * kD;
-            reinterpret_cast<float4 *>(dst)[lane] = x;
+            reinterpret_cast<float4 *>(dst + (size_t)(warp * RPW + rr) * kD)[lane] = x;
         }
-        __syncwarp();
+        fence_proxy_async_smem();
+        if (tid == 0) bulk_wait_read0();   // the store of draft t-1 has read the other buffer
+        __syncthreads();
+        if (tid == 0) {
+            bulk_s2g(a.temp + ((((size_t)zi * N + t) * Hv + h) * kD + (size_t)tile * ROWS) * kD, dst, ROWS * kD * 4);
+            bulk_commit();
+        }
     }
+    if (tid == 0) bulk_wait_read0();   // shared memory stays live until the last store has read it
 }
 
 // Commit of the baseline: state <- temp[n_acc - 1] (Fig. 3).
@@ -214,21 +248,22 @@ static cudaError_t launch_rs(const RecArgs &a, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     return launch_k(kfn, dim3(kD / kRows, a.dm.Hk, a.n), dim3(256), smem, s, a.pdl != 0, a);
 }
-template <int G, typename InT>
+template <typename InT>
 static cudaError_t launch_rv(const RecArgs &a, cudaStream_t s) {
-    const size_t smem = 128 + (size_t)G * kRows * kD * 4 + 8 * 32 * 4;
-    auto kfn = recurrent_verify_kernel<InT, G>;
+    const size_t smem = 128 + 2 * (size_t)kRows * kD * 4 + (size_t)a.n_draft * (2 * kD + kRows) * sizeof(InT) + 48 * 4;
+    auto kfn = recurrent_verify_kernel<InT>;
     cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    return launch_k(kfn, dim3(kD / kRows, a.dm.Hk, a.n), dim3(256), smem, s, a.pdl != 0, a);
+    return launch_k(kfn, dim3(kD / kRows, a.dm.Hv, a.n), dim3(128), smem, s, a.pdl != 0, a);
 }
 
 template <typename InT>
 static cudaError_t dispatch_step(const RecArgs &a, cudaStream_t s, bool verify) {
+    if (verify) return launch_rv<InT>(a, s);
     switch (a.dm.g) {
-        case 1: return verify ? launch_rv<1, InT>(a, s) : launch_rs<1, InT>(a, s);
-        case 2: return verify ? launch_rv<2, InT>(a, s) : launch_rs<2, InT>(a, s);
-        case 4: return verify ? launch_rv<4, InT>(a, s) : launch_rs<4, InT>(a, s);
+        case 1: return launch_rs<1, InT>(a, s);
+        case 2: return launch_rs<2, InT>(a, s);
+        case 4: return launch_rs<4, InT>(a, s);
         default: return cudaErrorInvalidValue;
     }
 }
