@@ -38,7 +38,7 @@ UNIT = "tokens/s (one GDN layer, all GPUs)"
 D = 128
 
 
-def parse_args():
+def parse_args(argv=None):
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=60)
@@ -57,8 +57,67 @@ def parse_args():
     p.add_argument("--no-overlap", action="store_true", help="launch without PDL (la_set_overlap 0)")
     p.add_argument("--auto-flush", action="store_true",
                    help="headline WITH the fused flush (la_set_auto_flush; measured slower, see DESIGN.md)")
+    p.add_argument("--parallel", default="dp", choices=["dp", "tp"],
+                   help="dp: requests partitioned over ranks (headline, no collective); tp: heads partitioned, "
+                        "one la_tp_allgather of the head outputs per layer per step (P:232)")
+    p.add_argument("--no-config1", action="store_true", help="skip the config-1 latency row")
+    p.add_argument("--no-config5", action="store_true", help="skip the config-5 36-layer stack row")
     p.add_argument("--seed", type=int, default=1002)
-    return p.parse_args()
+    return p.parse_args(argv)
+
+
+# ---------------------------------------------------------------- ranks
+def free_port():
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def spawn_command(args, argv, env):
+    """`--gpus N` (N > 1) outside a torchrun environment: the command that
+    relaunches this script with one process per GPU (the driver's own
+    launch form), else None."""
+    if args.gpus <= 1 or "WORLD_SIZE" in env:
+        return None
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+            "--master-addr", "127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__), *argv]
+
+
+def rank_env(env=None):
+    """(world, rank, local_rank) from the torchrun environment (1, 0, 0 alone)."""
+    env = os.environ if env is None else env
+    return int(env.get("WORLD_SIZE", "1")), int(env.get("RANK", "0")), int(env.get("LOCAL_RANK", "0"))
+
+
+def check_world(args, world):
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but the launcher started {world} rank(s)")
+
+
+def rank_seed(args, rank):
+    """Per-rank input seed: each rank draws its own shard of the global batch."""
+    return args.seed * 1000 + 100 * rank
+
+
+def whole_job_value(world, batch_per_rank, us_per_token, parallel="dp"):
+    """tokens/s of one GDN layer over all ranks: DP serves world x batch
+    requests per step, TP serves one batch (heads split over the ranks)."""
+    served = batch_per_rank * (world if parallel == "dp" else 1)
+    return served / (us_per_token * 1e-6)
+
+
+def cpu_model():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
 
 
 # ---------------------------------------------------------------- clocks
@@ -195,23 +254,24 @@ def capture(torch, stream, fn):
 def cpu_oracle_sample(target_s=15.0, B=64, Hk=16, Hv=32, seed=1002, max_tok=None):
     """Time the fp64 oracle (the recurrence, as it stands) on host cores on a
     bounded sample of the config-2 workload: B slots x Hv heads x T tokens from
-    synthetic 32K-context states.  Returns (tokens/s, cores, sample text)."""
+    synthetic 32K-context states.  Returns a cpu_baseline dict: tokens/s on all
+    cores, the same on ONE thread (a smaller sample), cores, CPU model."""
     import numpy as np
     import oracle
     import synth
     rc = synth.Recipe(seed=seed)
-    slots = np.arange(B)
-    S0 = synth.state0(rc, slots, Hv, D, D).astype(np.float64).reshape(B * Hv, D, D)
     cores = oracle.default_threads()
 
-    def run(T):
+    def run(T, nslots=B, threads=cores):
+        slots = np.arange(nslots)
+        S0 = synth.state0(rc, slots, Hv, D, D).astype(np.float64).reshape(nslots * Hv, D, D)
         tok = synth.tokens(rc, slots, np.arange(T), Hk, Hv, D)
         qv = synth.expand_qk_to_v_heads(tok["q"], Hv)
         kv = synth.expand_qk_to_v_heads(tok["k"], Hv)
-        seq = lambda x: np.ascontiguousarray(np.swapaxes(x, 1, 2).reshape((B * Hv, T) + x.shape[3:]))
+        seq = lambda x: np.ascontiguousarray(np.swapaxes(x, 1, 2).reshape((nslots * Hv, T) + x.shape[3:]))
         args = [seq(qv), seq(kv), seq(tok["v"]), seq(tok["alpha"]), seq(tok["beta"])]
         t0 = time.perf_counter()
-        oracle.gdn_run(S0, *args, n_threads=cores)
+        oracle.gdn_run(S0, *args, n_threads=threads)
         return time.perf_counter() - t0
 
     # calibrate: per-call overhead (state copy-in) + per-token cost, then one
@@ -222,7 +282,13 @@ def cpu_oracle_sample(target_s=15.0, B=64, Hk=16, Hv=32, seed=1002, max_tok=None
     if max_tok:
         T = min(T, max_tok)
     dt = run(T)
-    return B * T / dt, cores, f"{B} slots x {Hv} V heads x {T} tokens (config 2 shape, fp64 recurrence, {dt:.1f} s)"
+    # single thread: 16 slots x 32 tokens (same per-token work)
+    t1 = run(32, nslots=16, threads=1)
+    return {"value": B * T / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "cpu_model": cpu_model(),
+            "sample": f"{B} slots x {Hv} V heads x {T} tokens (config 2 shape, fp64 recurrence, {dt:.1f} s)",
+            "single_thread": {"value": 16 * 32 / t1, "unit": UNIT, "cores": 1,
+                              "sample": f"16 slots x {Hv} V heads x 32 tokens ({t1:.2f} s)"}}
 
 
 # ---------------------------------------------------------------- reference arm
@@ -267,14 +333,21 @@ def run_reference(args):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": "config2: Qwen3-Next GDN layer decode, batch 64 @32K ctx (CPU oracle sample)",
                        "batch_per_gpu": B, "chunk": args.chunk},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample,
+                             "cpu_model": cpu_model()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
 # ---------------------------------------------------------------- main arm
-def main():
-    args = parse_args()
+def main(argv=None):
+    argv = sys.argv[1:] if argv is None else argv
+    args = parse_args(argv)
+    cmd = spawn_command(args, argv, os.environ)
+    if cmd:   # one process per GPU, launched like the driver does
+        sys.exit(subprocess.call(cmd))
+    world, rank, local = rank_env()
+    check_world(args, world)
     if args.impl == "reference":
         run_reference(args)
         return
@@ -283,9 +356,6 @@ def main():
     from paper_2605_19049_b200 import cost
     from paper_2605_19049_b200 import labuf as L
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -304,7 +374,18 @@ def main():
 
     B, C, NL, Hk, Hv = args.batch, args.chunk, args.layers, 16, 32
     K, W = args.steps, max(3, args.warmup)
-    seed0 = args.seed * 1000 + 100 * rank      # per-rank inputs: this rank's shard of the global batch
+    seed0 = rank_seed(args, rank)              # per-rank inputs: this rank's shard of the global batch
+    tp = args.parallel == "tp"
+    comm = None
+    if tp:
+        # tensor parallel over heads: this rank owns QK heads [q0, q0 + Hk/G) and
+        # their V heads for ALL requests; head outputs are all-gathered per layer
+        _, Hk, _, Hv = dp.head_range(16, 32, rank, world)
+        uid = [L.tp_unique_id() if rank == 0 else None]
+        if world > 1:
+            dist.broadcast_object_list(uid, src=0)
+        comm = L.TPComm(uid[0], rank, world, dev.index)
+        gathered = [torch.empty(world, B, Hv, D, dtype=torch.float32, device=dev) for _ in range(NL)]
     clocks = ClockSampler(dev.index if world == 1 else local)
     clocks.start()
     peak, peak_src = measured_peaks()
@@ -330,6 +411,8 @@ def main():
             for l, b in enumerate(bufs):
                 x = inputs[t][l]
                 b.decode_step(0, x["q"], x["k"], x["v"], x["alpha"], x["beta"], x["o"])
+                if tp:   # the layer's head outputs, gathered before the next layer could run
+                    comm.allgather(x["o"], gathered[l])
 
     def flush_phase():
         for b in bufs:
@@ -372,7 +455,7 @@ def main():
     total_ms = max_over_ranks(total_ms)
     ms_per_step = total_ms / K
     us_per_token = 1e3 * ms_per_step / (C * NL)          # one decode step of one layer, cycle avg
-    value = world * B / (us_per_token * 1e-6)
+    value = whole_job_value(world, B, us_per_token, args.parallel)
 
     # ---- recurrent baseline (kernel 5a), same tokens, same layers
     def rec_phase():
@@ -380,6 +463,8 @@ def main():
             for l, b in enumerate(bufs):
                 x = inputs[t][l]
                 b.recurrent_step(0, x["q"], x["k"], x["v"], x["alpha"], x["beta"], x["o"])
+                if tp:
+                    comm.allgather(x["o"], gathered[l])
 
     g_rec = capture(torch, stream, rec_phase)
     barrier()
@@ -412,12 +497,17 @@ def main():
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
-        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong" if tp else "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": "config2: Qwen3-Next GDN layer decode, batch 64/GPU @32K ctx (synthetic state), C=16",
-                   "batch_per_gpu": B, "global_batch": B * world, "chunk": C, "layers_rotated": NL,
+        "config": {"workload": (f"config2: Qwen3-Next GDN layer decode, batch {B} @32K ctx (synthetic state), C={C}, "
+                                f"heads split over {world} rank(s)" if tp else
+                                f"config2: Qwen3-Next GDN layer decode, batch {B}/GPU @32K ctx (synthetic state), C={C}"),
+                   "batch_per_gpu": B, "global_batch": B if tp else B * world, "chunk": C, "layers_rotated": NL,
                    "heads": {"qk": Hk, "v": Hv, "d": D}, "in_dtype": args.in_dtype, "u_dtype": args.u_dtype,
-                   "state": "fp32", "parallelism": f"dp{world} (requests partitioned, no collective)",
+                   "state": "fp32",
+                   "parallelism": (f"tp{world} (heads partitioned; one la_tp_allgather (NCCL) of the head outputs "
+                                   f"per layer per step, not overlapped, inside the timed region)" if tp else
+                                   f"dp{world} (requests partitioned, no collective)"),
                    "step": (f"one buffer cycle: {C} decode steps, the last folding the buffer in-kernel "
                             f"(fused flush), x {NL} layer instances" if auto else
                             f"one buffer cycle: {C} decode steps + 1 flush, x {NL} layer instances"),
@@ -425,7 +515,7 @@ def main():
                    "l2": f"inputs larger than L2: {NL} layers x {B * lb.st / 2**20:.0f} MiB state rotated per step",
                    "cuda_graphs": True, "launch_overlap": not args.no_overlap},
         "us_per_token": us_per_token,
-        "tokens_per_s_per_gpu": B / (us_per_token * 1e-6),
+        "tokens_per_s_per_gpu": value / world,
         "hbm_frac_of_8TBs": step_bytes / (ms_per_step * 1e-3) / 8e12,
         "hbm_frac_of_measured": step_bytes / (ms_per_step * 1e-3) / (peak * 1e9),
         "recurrent": {"us_per_token": rec_us_per_token,
@@ -494,9 +584,12 @@ def main():
         offs, per_layer = carve(in_nb)
         o_nb = B * Hv * D * 4
         dev_in = [torch.empty(NL * per_layer, dtype=torch.uint8, device=dev) for _ in range(C)]
-        dev_out = [torch.empty(NL, B, Hv, D, dtype=torch.float32, device=dev) for _ in range(C)]
+        # TP: each layer's gathered head outputs of all ranks come back
+        osh = (NL, world, B, Hv, D) if tp else (NL, B, Hv, D)
+        dev_out = [torch.empty(osh, dtype=torch.float32, device=dev) for _ in range(C)]
+        host_out = [torch.empty(osh, dtype=torch.float32).pin_memory() for _ in range(C)]
+        o_loc = [torch.empty(B, Hv, D, dtype=torch.float32, device=dev) for _ in range(NL)] if tp else None
         host_in = [torch.empty(NL * per_layer, dtype=torch.uint8).pin_memory() for _ in range(C)]
-        host_out = [torch.empty(NL, B, Hv, D, dtype=torch.float32).pin_memory() for _ in range(C)]
         views = []
         for t in range(C):
             row = []
@@ -506,7 +599,7 @@ def main():
                     base = l * per_layer + off
                     v[k_] = dev_in[t][base:base + nb].view(dt).view(sh)
                     v[k_].copy_(inputs[t][l][k_])                    # the same values as the device-resident run
-                v["o"] = dev_out[t][l]
+                v["o"] = o_loc[l] if tp else dev_out[t][l]
                 row.append(v)
             views.append(row)
             host_in[t].copy_(dev_in[t])
@@ -530,6 +623,8 @@ def main():
                 for l, b in enumerate(bufs):
                     x = views[t][l]
                     b.decode_step(0, x["q"], x["k"], x["v"], x["alpha"], x["beta"], x["o"])
+                    if tp:
+                        comm.allgather(x["o"], dev_out[t][l])
                 ev_out[t].record(stream)
             for b in bufs:
                 b.flush(0, B, L.LA_FLUSH_FULL)
@@ -555,9 +650,26 @@ def main():
         # the outputs really came back: the last step's host copy equals the device outputs
         e2e_ok = bool(torch.equal(host_out[C - 1], dev_out[C - 1].cpu()))
         e2e_us_tok = 1e6 * e2e_s / K_e2e / (C * NL)
-        line["e2e"] = {"value": world * B / (e2e_us_tok * 1e-6), "unit": UNIT,
+        # the same step issued eagerly: every la_* call (validation, host
+        # mirror, launch) and every copy is issued by the host each step
+        with torch.cuda.stream(stream):
+            e2e_step()
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(K_e2e):
+            with torch.cuda.stream(stream):
+                e2e_step()
+        barrier()
+        eager_s = max_over_ranks(time.perf_counter() - t0)
+        eager_ok = bool(torch.equal(host_out[C - 1], dev_out[C - 1].cpu()))
+        eager_us_tok = 1e6 * eager_s / K_e2e / (C * NL)
+        line["e2e"] = {"value": whole_job_value(world, B, e2e_us_tok, args.parallel), "unit": UNIT,
                        "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                        "steps": K_e2e, "outputs_checked": e2e_ok,
+                       "eager": {"value": whole_job_value(world, B, eager_us_tok, args.parallel), "unit": UNIT,
+                                 "outputs_checked": eager_ok,
+                                 "note": "the same step without a CUDA graph: the host issues every la_* call "
+                                         "and every copy each step"},
                        "note": "la_* calls through the public binding with pinned host buffers: H2D of every "
                                "step's q/k/v/alpha/beta and D2H of every output inside the timed region (16 + 16 "
                                "contiguous copies per step on two copy streams beside the decodes; the step is "
@@ -565,7 +677,7 @@ def main():
         del g_e2e, dev_in, dev_out, views
 
     # ---- extra rows: verify + commit (config 3) and direct (config 4)
-    if not args.no_rows:
+    if not args.no_rows and not tp:
         del g_rec
         line["rows"] = extra_rows(torch, L, cost, dev, stream, seed0 + 5000, K, W, peak, args)
 
@@ -574,10 +686,11 @@ def main():
     line["clocks"] = clocks.summary(t_c0, t_c2)
 
     if rank == 0 and world == 1 and not args.no_cpu:
-        v, cores, sample = cpu_oracle_sample(seed=args.seed)
-        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample}
+        line["cpu_baseline"] = cpu_oracle_sample(seed=args.seed)
     if rank == 0:
         print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.destroy()
     if world > 1:
         dist.destroy_process_group()
 
@@ -748,15 +861,176 @@ def extra_rows(torch, L, cost, dev, stream, seed, K, W, peak, args):
         torch.cuda.synchronize()
         r_ms.append(e0.elapsed_time(e1))
     r_us = 1e3 * min(r_ms) / NS
+    # Fig. 7 analogue: direct at context L (8 steps from L) vs chunkwise C = 16
+    # (cycle of 16 decodes + the flush, same batch) vs recurrent
+    fig7 = []
+    for Lc in (16, 32, 64, 96, 120):
+        x0 = sd.tokens(seed + 60 + Lc, B4, Lc, Hk, Hv, D, device=dev)
+        x0["o"] = torch.empty(B4, Lc, Hv, D, dtype=torch.float32, device=dev)
+        b4.reset(mode=L.LA_MODE_DIRECT, zero_state=False)
+        b4.direct_short(0, x0["q"], x0["k"], x0["v"], x0["alpha"], x0["beta"], x0["o"])
+        torch.cuda.synchronize()
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+            for x in steps[:8]:
+                b4.direct_short(0, x["q"], x["k"], x["v"], x["alpha"], x["beta"], x["o"])
+            e1.record(stream)
+        torch.cuda.synchronize()
+        du = 1e3 * e0.elapsed_time(e1) / 8
+        db = B4 * sum(lb4.direct(Lc + s_) for s_ in range(8)) / 8
+        fig7.append({"context": Lc + 4, "direct_us_per_step": du, "direct_frac_of_measured": gbs(db, du) / peak})
+        del x0
+    del b4
+    torch.cuda.empty_cache()
+    # chunkwise C = 16 at the same batch (one layer: 2 GiB of state > L2)
+    cfgc = L.make_config(B4, Hk, Hv, chunk=16, u_dtype="f16")
+    bc = L.LaBuf(cfgc, device=dev)
+    bc.set_overlap(not args.no_overlap)
+    bc.reset(zero_state=True)
+
+    def cyc():
+        for x in sq[:16]:
+            bc.decode_step(0, x["q"], x["k"], x["v"], x["alpha"], x["beta"], x["o"])
+        bc.flush(0, B4, L.LA_FLUSH_FULL)
+    gcy = capture(torch, stream, cyc)
+    _, (cy_ms,) = timed_graphs(torch, stream, [gcy], 5, 3)
+    chunk_us = 1e3 * cy_ms / 5 / 16
+    for row in fig7:
+        row["chunkwise_c16_us_per_token"] = chunk_us
+        row["recurrent_us_per_step"] = r_us
+        row["direct_vs_chunkwise"] = chunk_us / row["direct_us_per_step"]
+        row["paper_model_direct_vs_chunkwise"] = float(cost.paper_speedup_kv_only_gdn(D, 16, row["context"]))
+    del gcy, bc
     rows["direct"] = {
         "workload": f"config4: batch {B4}, direct KV-only decode from context {L0} to {L0 + NS}, u fp16, no state",
         "us_per_step": d_us, "gbs": gbs(d_bytes, d_us), "frac_of_measured": gbs(d_bytes, d_us) / peak,
         "recurrent_us_per_step": r_us, "speedup_vs_recurrent": r_us / d_us,
+        "chunkwise_c16_us_per_token": chunk_us, "speedup_vs_chunkwise": chunk_us / d_us,
         "paper_model_speedup_vs_chunkwise_m16_at_L80": float(cost.paper_speedup_kv_only_gdn(D, 16, L0 + NS // 2)),
+        "fig7": fig7,
+        "fig7_note": "batch 1024, u fp16; direct at context L..L+8 vs the chunkwise C = 16 cycle (u fp16) and "
+                     "the recurrent step at the same batch; the paper's claim is direct ~ chunkwise near L = d "
+                     "(P:287-290, Eq. 10 P:212)",
     }
-    del b4, br
+    del br
     torch.cuda.empty_cache()
+    if not args.no_config1:
+        rows["config1"] = row_config1(torch, L, sd, dev, stream, seed + 70)
+    if not args.no_config5:
+        try:
+            rows["config5"] = row_config5(torch, L, cost, sd, dev, seed + 80, peak, args)
+        except torch.cuda.OutOfMemoryError as e:
+            rows["config5"] = {"error": f"out of memory: {e}"[:300]}
+        torch.cuda.empty_cache()
     return rows
+
+
+def row_config1(torch, L, sd, dev, stream, seed):
+    """Config 1 (BASELINE configs[0]): 1 request, 1 GDN head, d = 128, fp32,
+    64-token prefill + 64 decode steps, C = 16, vs the recurrent kernel: the
+    batch-1 latency regime where launches, not bytes, set the time."""
+    cfg = L.make_config(1, 1, 1, chunk=16, in_dtype="f32")
+    b = L.LaBuf(cfg, device=dev)
+    b.set_overlap(True)
+    b.reset(zero_state=True)
+    pre = sd.tokens(seed, 1, 64, 1, 1, D, in_dtype="f32", device=dev)
+    pre_o = torch.empty(1, 64, 1, D, dtype=torch.float32, device=dev)
+    xs = [sd.tokens(seed + 1 + t, 1, 1, 1, 1, D, in_dtype="f32", device=dev, squeeze=True) for t in range(16)]
+    for x in xs:
+        x["o"] = torch.empty(1, 1, D, dtype=torch.float32, device=dev)
+    g_pre = capture(torch, stream, lambda: b.prefill(0, pre["q"], pre["k"], pre["v"], pre["alpha"], pre["beta"], pre_o))
+    _, (pre_ms,) = timed_graphs(torch, stream, [g_pre], 20, 3)
+
+    def cyc():
+        for x in xs:
+            b.decode_step(0, x["q"], x["k"], x["v"], x["alpha"], x["beta"], x["o"])
+        b.flush(0, 1, L.LA_FLUSH_FULL)
+
+    def rec():
+        for x in xs:
+            b.recurrent_step(0, x["q"], x["k"], x["v"], x["alpha"], x["beta"], x["o"])
+    g_cyc, g_rec = capture(torch, stream, cyc), capture(torch, stream, rec)
+    _, (cyc_ms,) = timed_graphs(torch, stream, [g_cyc], 50, 5)
+    _, (rec_ms,) = timed_graphs(torch, stream, [g_rec], 50, 5)
+    buf_us, rec_us = 1e3 * cyc_ms / 50 / 16, 1e3 * rec_ms / 50 / 16
+    return {"workload": "config1: 1 request, 1 head, d=128, fp32, 64-token prefill + decode cycles of C=16 "
+                        "(16 decodes + flush, one CUDA graph) vs 16 recurrent steps",
+            "prefill_64_us": 1e3 * pre_ms / 20,
+            "buffered_us_per_token": buf_us, "recurrent_us_per_token": rec_us,
+            "speedup_vs_recurrent": rec_us / buf_us,
+            "note": "launch-bound: one head is 133 KB per recurrent token; the paper notes the batch-1 penalty "
+                    "(P:256)"}
+
+
+def row_config5(torch, L, cost, sd, dev, seed, peak, args):
+    """Config 5 (BASELINE configs[4]): 36 stacked GDN layers, 2048 mixed
+    requests (1536 long: buffered decode C = 16, occupancies staggered; 512
+    short: KV-only, no state, L0 in {16, 40, 64, 96}) — this rank's DP shard
+    — 32 decode steps through paper_2605_19049_b200.stack, eager launches."""
+    from paper_2605_19049_b200 import dp
+    from paper_2605_19049_b200.stack import GdnStack, StackSpec, long_groups, short_groups
+    world, rank, _ = rank_env()
+    sh = dp.mixed_assignment(1536, 512, rank, world)
+    spec = StackSpec(n_layers=36, n_long=len(sh.long_ids), n_short=len(sh.short_ids))
+    Hk, Hv, NS = spec.n_qk_heads, spec.n_v_heads, 32
+    need = GdnStack.footprint_of(spec)
+    free = torch.cuda.mem_get_info(dev)[0]
+    if need > 0.97 * free:
+        return {"error": f"does not fit: la_buf_query footprint {need / 1e9:.1f} GB > {free / 1e9:.1f} GB free",
+                "footprint_bytes_la_buf_query": need}
+    st = GdnStack.create(spec, dev)
+    foot = st.footprint_bytes()
+    for l, lay in enumerate(st.layers):
+        lay.long.reset(zero_state=False)
+        lay.long.state.copy_(sd.state0(seed + l, spec.n_long, Hv, device=dev))
+        lay.short.reset(mode=L.LA_MODE_DIRECT, zero_state=False)
+        lay.long.set_overlap(True)
+        lay.short.set_overlap(True)
+    # one set of decode inputs per layer (reused over the steps: 36 layers of
+    # inputs exceed L2, and the values do not change the work)
+    lin = [sd.tokens(seed + 100 + l, spec.n_long, 1, Hk, Hv, D, device=dev, squeeze=True) for l in range(36)]
+    sin = [sd.tokens(seed + 200 + l, spec.n_short, 1, Hk, Hv, D, device=dev, in_dtype="bf16") for l in range(36)]
+    lout = [torch.empty(spec.n_long, Hv, D, dtype=torch.float32, device=dev) for _ in range(36)]
+    sout = [torch.empty(spec.n_short, 1, Hv, D, dtype=torch.float32, device=dev) for _ in range(36)]
+    pre = {}
+
+    def short_tok(l, g):
+        f, m, l0 = short_groups(spec)[g]
+        key = (m, l0)
+        if key not in pre:
+            pre[key] = sd.tokens(seed + 300 + l0, m, l0, Hk, Hv, D, device=dev)
+        return pre[key]
+    st.warmup(lambda l, t: lin[l], short_tok)
+    pre.clear()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = sum(lay.long.kernel_launches() + lay.short.kernel_launches() for lay in st.layers)
+    stream = torch.cuda.current_stream(dev)
+    e0.record(stream)
+    for _ in range(NS):
+        st.step(lin, sin, lout, sout)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    launches = sum(lay.long.kernel_launches() + lay.short.kernel_launches() for lay in st.layers) - launches0
+    ms = e0.elapsed_time(e1) / NS
+    finite = bool(torch.isfinite(lout[-1]).all() and torch.isfinite(sout[-1]).all())
+    # algorithmic bytes per stack step: long slots average one full cycle
+    # (32 steps = 2 cycles of C = 16), short slots at their contexts
+    lbl = cost.LayerBytes.make(Hk, Hv, D, 2, 4)
+    lbs = cost.LayerBytes.make(Hk, Hv, D, 2, 2)
+    long_b = spec.n_long * float(lbl.cycle_avg(spec.chunk))
+    short_b = sum(m * sum(lbs.direct(l0 + s_) for s_ in range(NS)) / NS for _, m, l0 in short_groups(spec))
+    step_bytes = 36 * (long_b + short_b)
+    n_tok = spec.n_long + spec.n_short
+    return {"workload": f"config5: 36 Qwen3-Next GDN layers, {n_tok} of 2048 mixed requests on this rank "
+                        f"({spec.n_long} long buffered C=16 staggered, {spec.n_short} short KV-only), {NS} steps, "
+                        "eager launches (the short contexts grow every step, so no graph replay)",
+            "ms_per_step": ms, "tokens_per_s_per_gpu": n_tok / (ms * 1e-3),
+            "us_per_token_per_layer": 1e3 * ms / 36,
+            "footprint_bytes_la_buf_query": foot, "footprint_gb": foot / 1e9,
+            "algorithmic_bytes_per_step": step_bytes,
+            "hbm_frac_of_measured": step_bytes / (ms * 1e-3) / (peak * 1e9),
+            "kernel_launches_per_step": launches / NS, "outputs_finite": finite}
 
 
 if __name__ == "__main__":

@@ -60,6 +60,17 @@ def short_groups(spec: StackSpec):
     return out
 
 
+def _configs(spec: StackSpec):
+    """The per-layer handle configurations: long (chunkwise) [, short (direct)]."""
+    out = [L.make_config(spec.n_long, spec.n_qk_heads, spec.n_v_heads, chunk=spec.chunk,
+                         in_dtype=spec.in_dtype, u_dtype="f32", validate=False)]
+    if spec.n_short:
+        out.append(L.make_config(spec.n_short, spec.n_qk_heads, spec.n_v_heads, chunk=spec.chunk,
+                                 short_cap=spec.short_cap, in_dtype=spec.in_dtype,
+                                 u_dtype="f16" if spec.in_dtype == "bf16" else "f32", validate=False))
+    return out
+
+
 @dataclass
 class Layer:
     long: L.LaBuf
@@ -75,16 +86,10 @@ class GdnStack:
     @classmethod
     def create(cls, spec: StackSpec, device):
         st = cls(spec, torch.device(device))
+        cfgs = _configs(spec)
         for _ in range(spec.n_layers):
-            lc = L.make_config(spec.n_long, spec.n_qk_heads, spec.n_v_heads, chunk=spec.chunk,
-                               in_dtype=spec.in_dtype, u_dtype="f32", validate=False)
-            sb = None
-            if spec.n_short:
-                sc = L.make_config(spec.n_short, spec.n_qk_heads, spec.n_v_heads, chunk=spec.chunk,
-                                   short_cap=spec.short_cap, in_dtype=spec.in_dtype,
-                                   u_dtype="f16" if spec.in_dtype == "bf16" else "f32", validate=False)
-                sb = L.LaBuf(sc, device=st.device)
-            st.layers.append(Layer(L.LaBuf(lc, device=st.device), sb))
+            sb = L.LaBuf(cfgs[1], device=st.device) if len(cfgs) > 1 else None
+            st.layers.append(Layer(L.LaBuf(cfgs[0], device=st.device), sb))
         return st
 
     def reset(self, states):
@@ -138,6 +143,15 @@ class GdnStack:
             if lay.short is not None:
                 y = short_in[l]
                 lay.short.direct_short(0, y["q"], y["k"], y["v"], y["alpha"], y["beta"], short_out[l])
+
+    @staticmethod
+    def footprint_of(spec: StackSpec) -> int:
+        """Device bytes the stack would allocate (la_buf_query), before creating it."""
+        tot = 0
+        for cfg in _configs(spec):
+            sz = L.query(cfg)
+            tot += sz.state_bytes + sz.buffer_bytes + sz.meta_bytes
+        return tot * spec.n_layers
 
     def footprint_bytes(self):
         tot = 0
