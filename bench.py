@@ -965,69 +965,79 @@ def row_config1(torch, L, sd, dev, stream, seed):
 def row_config5(torch, L, cost, sd, dev, seed, peak, args):
     """Config 5 (BASELINE configs[4]): 36 stacked GDN layers, 2048 mixed
     requests (1536 long: buffered decode C = 16, occupancies staggered; 512
-    short: KV-only, no state, L0 in {16, 40, 64, 96}) — this rank's DP shard
-    — 32 decode steps through paper_2605_19049_b200.stack, eager launches."""
+    short: KV-only, no state, L0 in {16, 40, 64, 96}) -- this rank's DP shard
+    -- on ONE paged handle per layer (record blocks of 16 tokens, a state
+    pool for the long requests; paper_2605_19049_b200.stack.MixedStack):
+    32 decode steps, one la_decode_mixed per layer per step, eager launches."""
     from paper_2605_19049_b200 import dp
-    from paper_2605_19049_b200.stack import GdnStack, StackSpec, long_groups, short_groups
+    from paper_2605_19049_b200.stack import MixedStack, StackSpec, short_groups
     world, rank, _ = rank_env()
     sh = dp.mixed_assignment(1536, 512, rank, world)
     spec = StackSpec(n_layers=36, n_long=len(sh.long_ids), n_short=len(sh.short_ids))
     Hk, Hv, NS = spec.n_qk_heads, spec.n_v_heads, 32
-    need = GdnStack.footprint_of(spec)
+    n_tok = spec.n_long + spec.n_short
+    need = MixedStack.footprint_of(spec)
     free = torch.cuda.mem_get_info(dev)[0]
     if need > 0.97 * free:
         return {"error": f"does not fit: la_buf_query footprint {need / 1e9:.1f} GB > {free / 1e9:.1f} GB free",
                 "footprint_bytes_la_buf_query": need}
-    st = GdnStack.create(spec, dev)
+    st = MixedStack.create(spec, dev)
     foot = st.footprint_bytes()
-    for l, lay in enumerate(st.layers):
-        lay.long.reset(zero_state=False)
-        lay.long.state.copy_(sd.state0(seed + l, spec.n_long, Hv, device=dev))
-        lay.short.reset(mode=L.LA_MODE_DIRECT, zero_state=False)
-        lay.long.set_overlap(True)
-        lay.short.set_overlap(True)
+    st.reset([sd.state0(seed + l, spec.n_long, Hv, device=dev) for l in range(36)])
+    for b in st.layers:
+        b.set_overlap(True)
     # one set of decode inputs per layer (reused over the steps: 36 layers of
     # inputs exceed L2, and the values do not change the work)
-    lin = [sd.tokens(seed + 100 + l, spec.n_long, 1, Hk, Hv, D, device=dev, squeeze=True) for l in range(36)]
-    sin = [sd.tokens(seed + 200 + l, spec.n_short, 1, Hk, Hv, D, device=dev, in_dtype="bf16") for l in range(36)]
-    lout = [torch.empty(spec.n_long, Hv, D, dtype=torch.float32, device=dev) for _ in range(36)]
-    sout = [torch.empty(spec.n_short, 1, Hv, D, dtype=torch.float32, device=dev) for _ in range(36)]
+    xin = [sd.tokens(seed + 100 + l, n_tok, 1, Hk, Hv, D, device=dev, squeeze=True) for l in range(36)]
+    out = [torch.empty(n_tok, Hv, D, dtype=torch.float32, device=dev) for _ in range(36)]
     pre = {}
 
     def short_tok(l, g):
         f, m, l0 = short_groups(spec)[g]
-        key = (m, l0)
-        if key not in pre:
-            pre[key] = sd.tokens(seed + 300 + l0, m, l0, Hk, Hv, D, device=dev)
-        return pre[key]
-    st.warmup(lambda l, t: lin[l], short_tok)
+        if (m, l0) not in pre:
+            pre[(m, l0)] = sd.tokens(seed + 300 + l0, m, l0, Hk, Hv, D, device=dev)
+        return pre[(m, l0)]
+    st.warmup(lambda l, t: {k: v[:spec.n_long] for k, v in xin[l].items()}, short_tok)
     pre.clear()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    launches0 = sum(lay.long.kernel_launches() + lay.short.kernel_launches() for lay in st.layers)
+    launches0 = sum(b.kernel_launches() for b in st.layers)
     stream = torch.cuda.current_stream(dev)
+    st.step(xin, out)                      # one untimed step (first-touch of the work lists)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
     e0.record(stream)
     for _ in range(NS):
-        st.step(lin, sin, lout, sout)
+        st.step(xin, out)
     e1.record(stream)
     torch.cuda.synchronize()
-    launches = sum(lay.long.kernel_launches() + lay.short.kernel_launches() for lay in st.layers) - launches0
+    host_s = time.perf_counter() - t0
+    launches = sum(b.kernel_launches() for b in st.layers) - launches0
     ms = e0.elapsed_time(e1) / NS
-    finite = bool(torch.isfinite(lout[-1]).all() and torch.isfinite(sout[-1]).all())
-    # algorithmic bytes per stack step: long slots average one full cycle
-    # (32 steps = 2 cycles of C = 16), short slots at their contexts
-    lbl = cost.LayerBytes.make(Hk, Hv, D, 2, 4)
-    lbs = cost.LayerBytes.make(Hk, Hv, D, 2, 2)
-    long_b = spec.n_long * float(lbl.cycle_avg(spec.chunk))
-    short_b = sum(m * sum(lbs.direct(l0 + s_) for s_ in range(NS)) / NS for _, m, l0 in short_groups(spec))
+    finite = bool(torch.isfinite(out[-1]).all())
+    pool = st.layers[0].pool_info()
+    # algorithmic bytes per stack step (u fp16 records): long slots average one
+    # full cycle (32 steps = 2 cycles of C = 16), short slots at their contexts
+    lb = cost.LayerBytes.make(Hk, Hv, D, 2, 2)
+    long_b = spec.n_long * float(lb.cycle_avg(spec.chunk))
+    short_b = sum(m * sum(lb.direct(l0 + 1 + s_) for s_ in range(NS)) / NS for _, m, l0 in short_groups(spec))
     step_bytes = 36 * (long_b + short_b)
-    n_tok = spec.n_long + spec.n_short
+    two_handle = None
+    try:
+        from paper_2605_19049_b200.stack import GdnStack
+        two_handle = GdnStack.footprint_of(spec)
+    except Exception:
+        pass
+    del st, xin, out
     return {"workload": f"config5: 36 Qwen3-Next GDN layers, {n_tok} of 2048 mixed requests on this rank "
-                        f"({spec.n_long} long buffered C=16 staggered, {spec.n_short} short KV-only), {NS} steps, "
-                        "eager launches (the short contexts grow every step, so no graph replay)",
+                        f"({spec.n_long} long buffered C=16 staggered, {spec.n_short} short KV-only), {NS} steps; "
+                        "one paged handle per layer (16-token blocks, state pool), one la_decode_mixed per layer "
+                        "per step, eager launches",
             "ms_per_step": ms, "tokens_per_s_per_gpu": n_tok / (ms * 1e-3),
-            "us_per_token_per_layer": 1e3 * ms / 36,
+            "us_per_token_per_layer": 1e3 * ms / 36, "host_issue_ms_per_step": 1e3 * host_s / NS,
             "footprint_bytes_la_buf_query": foot, "footprint_gb": foot / 1e9,
+            "footprint_gb_two_handle_layout": None if two_handle is None else two_handle / 1e9,
+            "pool_layer0": pool,
             "algorithmic_bytes_per_step": step_bytes,
             "hbm_frac_of_measured": step_bytes / (ms * 1e-3) / (peak * 1e9),
             "kernel_launches_per_step": launches / NS, "outputs_finite": finite}

@@ -23,12 +23,24 @@
  * ---------------------------------------------------------------- layout
  * Device memory is caller-owned (allocate it with torch.empty or cudaMalloc;
  * sizes from la_buf_query).  All pointers are DEVICE pointers unless noted.
- *   state   fp32 [R][Hv][d_v][d_k]   (d_k contiguous; 64 KiB per (slot,head))
- *   buffer  one allocation holding, at offsets reported by la_buf_query:
- *           K [R][Hk][T][d_k] in_dtype, U [R][Hv][T][d_v] u_dtype,
- *           G [R][Hv][T] fp32, and when keep_raw: V [R][Hv][T][d_v] in_dtype,
- *           B [R][Hv][T] fp32;   T = max(chunk + max_drafts, short_cap)
- *   meta    int32 occ[R], len[R], mode[R], ticket[R], then uint32 status
+ *   state   fp32 [S][Hv][d_v][d_k]   (d_k contiguous; 64 KiB per (state,head));
+ *           S = R (state of slot r at index r) or, with a state pool
+ *           (state_slots > 0), S = state_slots states assigned to slots on
+ *           demand (state_slots = -1: no states, a KV-only handle)
+ *   buffer  the record blocks, at offsets reported by la_buf_query:
+ *           K [nb][Hk][bt][d_k] in_dtype, U [nb][Hv][d_v/32][bt][32] u_dtype,
+ *           G [nb][Hv][bt] fp32, and when keep_raw: V [nb][Hv][bt][d_v]
+ *           in_dtype, B [nb][Hv][bt] fp32.  Contiguous handles
+ *           (block_tokens = 0): nb = R, bt = T = max(chunk + max_drafts,
+ *           short_cap) rounded up to 4, block r = slot r's records.  Paged
+ *           handles (block_tokens > 0): nb = n_blocks blocks of
+ *           bt = block_tokens records from one pool; a slot holds the blocks
+ *           its records need (position p -> its block p / bt, offset p % bt),
+ *           allocated by the library on append and returned on reset/release
+ *   meta    int32 occ[R], len[R], mode[R], ticket[R], uint32 status, then
+ *           (at the offsets in la_sizes) the state index per slot, the block
+ *           table [R][max_blocks] and the work lists of index-array batches.
+ *           Must be zero-filled before la_buf_create.
  * Per-call tensors (row-major, batch = contiguous slot range [first, first+n)):
  *   q, k  [n][n_tok][Hk][d_k] in_dtype;  v [n][n_tok][Hv][d_v] in_dtype;
  *   alpha, beta fp32 [n][n_tok][Hv];   o fp32 [n][n_tok][Hv][d_v]
@@ -57,6 +69,13 @@
  *   a replayed graph must cover closed cycles (the mirror does not see
  *   replays).
  * Determinism: identical inputs give bit-identical outputs (no float atomics).
+ * Pools: block and state allocation is a host
+ *   decision (LIFO free lists over ascending ids, so the same call sequence
+ *   gives the same ids); the block table and state indices are delivered to
+ *   the device in stream order by a small staging kernel whose entries travel
+ *   as kernel parameters.  Pool exhaustion is LA_ERR_CAPACITY before anything
+ *   is enqueued.  Invariants: free + held = pool size (blocks and states); a
+ *   block or state is held by at most one slot.
  */
 #ifndef LABUF_LA_H
 #define LABUF_LA_H
@@ -121,6 +140,13 @@ typedef struct {
     int32_t u_dtype;     /* la_dtype of buffered u: F32, or F16 with BF16 in  */
     int32_t keep_raw;    /* 1: also store v and beta per record               */
     int32_t validate;    /* 1: device-side value checks -> status word        */
+    int32_t block_tokens;/* 0: contiguous per-slot records; else paged record
+                            blocks of this many tokens, a multiple of 4 in
+                            [4, 128] (the paper: 8 or 16; = C or N,
+                            P:224)                                          */
+    int32_t n_blocks;    /* paged: blocks in the pool (>= 1); else ignored    */
+    int32_t state_slots; /* 0: one state per slot; > 0: a pool of that many
+                            states, assigned on demand; -1: no states          */
 } la_config;
 
 typedef struct {
@@ -131,6 +157,11 @@ typedef struct {
     int32_t capacity;    /* T, records per (slot, head)                       */
     size_t off_k, off_u, off_g, off_v, off_b;   /* offsets inside `buffer`    */
     size_t record_bytes; /* bytes per record per slot-layer (all heads)       */
+    int32_t block_tokens;/* bt: records per block (T when contiguous)         */
+    int32_t n_blocks;    /* nb: blocks in the buffer (R when contiguous)      */
+    int32_t max_blocks;  /* blocks a slot can hold: ceil(T / bt)              */
+    int32_t n_states;    /* states in `state`                                 */
+    size_t off_sidx, off_btab, off_wl;   /* byte offsets inside `meta`        */
 } la_sizes;
 
 /* Sizing query; no device access.  LA_ERR_INVALID/UNSUPPORTED on bad config. */
@@ -145,9 +176,40 @@ LA_API la_status la_buf_create(const la_config *cfg, void *state, void *buffer, 
 LA_API la_status la_buf_destroy(la_buf *buf);   /* frees host memory only */
 
 /* Reset slots [first, first+n): occ = len = 0, mode as given, and (if
- * zero_state) the state set to 0.  Clears a pending verify. */
+ * zero_state) the state set to 0.  Clears a pending verify.  Paged handles:
+ * the slots' record blocks return to the pool.  State pool: a CHUNKWISE slot
+ * keeps or receives a state (LA_ERR_CAPACITY if the pool is empty), a DIRECT
+ * slot returns its state. */
 LA_API la_status la_request_reset(la_buf *buf, int32_t first, int32_t n, int32_t mode,
                            int32_t zero_state, la_stream stream);
+
+/* Release slots [first, first+n) (request finished): their record blocks and
+ * state return to the pools; the slots become empty DIRECT slots (len 0)
+ * that hold nothing.  Enqueues nothing unless the slots held something. */
+LA_API la_status la_request_release(la_buf *buf, int32_t first, int32_t n, la_stream stream);
+
+/* Mixed-form decode step over an index-array batch (SURVEY
+ * NEXT-3): slots[i] (HOST int32 [n], distinct) receives the token at row i
+ * of q, k, v [n][Hk|Hv][d], alpha, beta [n][Hv]; o[i] [Hv][d_v] gets its
+ * output.  Each slot decodes in its current form:
+ *   CHUNKWISE: buffered decode (kernel 1); a buffer it fills is folded at the
+ *              end of the call (kernel 2, eager flush, reading Z15);
+ *   DIRECT with len < short_cap: KV-only decode (kernel 4);
+ *   DIRECT with len == short_cap: first compressed into a state (fold with
+ *              S0 = 0: "once the context length L >= d ... compress"),
+ *              then decoded as CHUNKWISE.
+ * Blocks and states are taken from the pools as needed (LA_ERR_CAPACITY,
+ * all-or-nothing, if they run out).  Requires no pending verify and, for
+ * CHUNKWISE slots, occ < chunk. */
+LA_API la_status la_decode_mixed(la_buf *buf, int32_t n, const int32_t *slots, const void *q,
+                          const void *k, const void *v, const float *alpha, const float *beta,
+                          float *o, la_stream stream);
+
+/* Pool occupancy (host mirror, no device access): free / total blocks and
+ * states, and the blocks slot `slot` holds (slot < 0: skip). */
+LA_API la_status la_pool_info(la_buf *buf, int32_t *free_blocks, int32_t *total_blocks,
+                       int32_t *free_states, int32_t *total_states, int32_t slot,
+                       int32_t *slot_blocks, int32_t *slot_state);
 
 /* Buffered decode step, kernel (1).  For each slot in the
  * range (CHUNKWISE, occ < chunk, no pending verify): computes u_t and

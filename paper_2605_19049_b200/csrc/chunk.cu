@@ -194,14 +194,20 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
     constexpr bool KQ_REG = NT == 1;             // k_t, q_t chunks held in registers
     constexpr int isz = (int)sizeof(InT), usz = (int)sizeof(UT);
     static_assert(NT <= 32, "decay scan runs inside one warp");
+    static_assert(NTHR >= 64, "warp 0 requests the records, warp 1 the new tokens");
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int seg = lane & 3, team = lane >> 2, par = team & 1;
     const int wt = warp / WPT, half = warp % WPT;  // the warp's d_v tile and row block in it
     const Dims dm = a.dm;
-    const int T = dm.T, Hv = dm.Hv, Hk = dm.Hk;
+    const int Hv = dm.Hv, Hk = dm.Hk;
     const int tg = blockIdx.x, h = blockIdx.y, zi = blockIdx.z;
-    const int r = a.first + zi, hk = h / dm.g;
+    // index-array batches: the slot and the caller's input row of CTA row zi
+    // (staged by a previous grid: L2 loads, and never before the PDL wait --
+    // the host clears pdl_early for list launches)
+    const int r = a.slots ? __ldcg(a.slots + zi) : a.first + zi, hk = h / dm.g;
+    const int xrow = a.pos ? __ldcg(a.pos + zi) : zi;
+    const size_t sb = a.p.sidx ? (size_t)__ldcg(a.p.sidx + r) : (size_t)r;   // state slot
     const int tile0 = tg * TPC;                  // first 32-row d_v tile of the CTA
     const int n_new = a.n_new;
     const bool direct = (a.kind == CK_DIRECT);
@@ -233,7 +239,7 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
     const InT *qin = static_cast<const InT *>(a.q);
     const InT *kin = static_cast<const InT *>(a.k);
     const InT *vin = static_cast<const InT *>(a.v);
-    auto tok_of = [&](int t) { return (size_t)zi * a.tok_total + a.tok_offset + t; };
+    auto tok_of = [&](int t) { return (size_t)xrow * a.tok_total + a.tok_offset + t; };
 
     // ---- 0. Two mbarriers.  `full`: the fixed-size operands (state tiles,
     //         new tokens), requested at once (thread 0: the state, warp 1:
@@ -247,11 +253,11 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
                                  (uint32_t)(n_new * (2 * kD * isz + TPC * 32 * isz));
     auto issue_state = [&]() {
         if constexpr (TC) {   // four 128-row x 32-column boxes, 128-byte swizzle
-            const int row0 = (r * Hv + h) * kD;
+            const int row0 = (int)((sb * Hv + h) * kD);
 #pragma unroll
             for (int kb = 0; kb < 4; ++kb) tma_load_2d(S_base + kb * (TPC * 32 * 128), &tmap, kb * 32, row0, full);
         } else {
-            bulk_g2s(smem + L.S, a.p.state + (((size_t)r * Hv + h) * kD + (size_t)tile0 * 32) * kD,
+            bulk_g2s(smem + L.S, a.p.state + ((sb * Hv + h) * kD + (size_t)tile0 * 32) * kD,
                      TPC * 32 * kD * 4, full);
         }
     };
@@ -280,31 +286,48 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
     }
     __syncthreads();
     int ticket = 0;
-    if (tid == 0) {
-        if (!(HAS_STATE && a.pdl_early)) {
-            mbar_arrive_expect_tx(full, fixed_bytes);
-            if (HAS_STATE) issue_state();
+    if (warp == 0) {
+        // lane 0: the state (unless early), the slot's count j0; the j0-dependent
+        // records are requested by the lanes in parallel, one copy per (record
+        // block, field): the tiles' u sub-tiles, the QK head's key rows, the
+        // log decays (contiguous handles: a single block)
+        int j0v = 0;
+        if (lane == 0) {
+            if (!(HAS_STATE && a.pdl_early)) {
+                mbar_arrive_expect_tx(full, fixed_bytes);
+                if (HAS_STATE) issue_state();
+            }
+            j0v = (direct ? a.p.len : a.p.occ)[r] + a.j_add;
+            *j0_s = j0v;
         }
-        const int j0v = (direct ? a.p.len : a.p.occ)[r] + a.j_add;
-        const int jbv = (j0v + 3) & ~3;
-        *j0_s = j0v;
-        mbar_arrive_expect_tx(recs, (uint32_t)(TPC * 32 * j0v * usz) + (uint32_t)(j0v * kD * isz) +
-                                        (j0v ? (uint32_t)(jbv * 4) : 0u));
-        if (j0v) {
-            for (int x = 0; x < TPC; ++x)
-                bulk_g2s(smem + L.U + (size_t)x * j0v * kUSub * usz,
-                         static_cast<const UT *>(a.p.U) + ((((size_t)r * Hv + h) * (kD / kUSub) + tile0 + x) * T) * kUSub,
-                         (uint32_t)(j0v * kUSub * usz), recs);
-            bulk_g2s(smem + L.K, static_cast<const InT *>(a.p.K) + ((size_t)r * Hk + hk) * T * kD,
-                     (uint32_t)(j0v * kD * isz), recs);
-            bulk_g2s(smem + L.Gs, a.p.G + ((size_t)r * Hv + h) * T, (uint32_t)(jbv * 4), recs);
+        j0v = __shfl_sync(0xffffffffu, j0v, 0);
+        const int bt = dm.bt, nb = (j0v + bt - 1) / bt;
+        if (lane == 0) {
+            uint32_t gbytes = 0;
+            for (int b = 0; b < nb; ++b) gbytes += (uint32_t)(((min(bt, j0v - b * bt) + 3) & ~3) * 4);
+            mbar_arrive_expect_tx(recs, (uint32_t)(TPC * 32 * j0v * usz) + (uint32_t)(j0v * kD * isz) + gbytes);
         }
-        if (a.kind != CK_VERIFY) ticket = atomicAdd(&a.p.ticket[r], 1);
-    } else if (NTHR == 32 || warp == 1) {
+        __syncwarp();
+        constexpr int NF = TPC + 2;
+        for (int c = lane; c < nb * NF; c += 32) {
+            const int b = c / NF, f = c % NF, cnt = min(bt, j0v - b * bt);
+            const size_t blk = a.p.btab ? (size_t)__ldcg(a.p.btab + (size_t)r * dm.maxb + b) : (size_t)r;
+            if (f < TPC)
+                bulk_g2s(smem + L.U + ((size_t)f * j0v + (size_t)b * bt) * kUSub * usz,
+                         static_cast<const UT *>(a.p.U) + (((blk * Hv + h) * (kD / kUSub) + tile0 + f) * bt) * kUSub,
+                         (uint32_t)(cnt * kUSub * usz), recs);
+            else if (f == TPC)
+                bulk_g2s(smem + L.K + (size_t)b * bt * kD * isz,
+                         static_cast<const InT *>(a.p.K) + (blk * Hk + hk) * bt * kD, (uint32_t)(cnt * kD * isz), recs);
+            else
+                bulk_g2s(smem + L.Gs + (size_t)b * bt * 4, a.p.G + (blk * Hv + h) * bt,
+                         (uint32_t)(((cnt + 3) & ~3) * 4), recs);
+        }
+        if (lane == 0 && a.kind != CK_VERIFY) ticket = atomicAdd(&a.p.ticket[r], 1);
+    } else if (warp == 1) {
         // new tokens: q_t, k_t rows of the QK head and the tiles' v_t slice
-        // (warp 1's lanes, so they issue in parallel with thread 0)
-        const int c0 = NTHR == 32 ? tid - 1 : lane, cs = NTHR == 32 ? 31 : 32;
-        for (int c = c0; c < 3 * n_new; c += cs) {
+        // (warp 1's lanes, so they issue in parallel with warp 0)
+        for (int c = lane; c < 3 * n_new; c += 32) {
             const int t = c % n_new, kind = c / n_new;
             if (kind == 0)
                 bulk_g2s(smem + L.q + (size_t)t * kD * isz, qin + (tok_of(t) * Hk + hk) * kD, kD * isz, full);
@@ -590,7 +613,11 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
         const int sub = lane / RPW, row = half * RPW + lane % RPW, tile = tile0 + wt;
         const int drow = tile * 32 + row;
         const UT *ut = U_s + (size_t)wt * j0 * kUSub + row;
-        UT *Uout = static_cast<UT *>(a.p.U) + ((((size_t)r * Hv + h) * (kD / kUSub) + tile) * T + j0) * kUSub + row;
+        // record position j0 + t of the slot: (block, offset)
+        auto recpos = [&](int t) -> int2 {
+            if (!a.p.btab) return make_int2(r, j0 + t);
+            return make_int2(__ldcg(a.p.btab + (size_t)r * dm.maxb + (j0 + t) / dm.bt), (j0 + t) % dm.bt);
+        };
         float un[NT];
 #pragma unroll
         for (int t = 0; t < NT; ++t) {
@@ -640,11 +667,12 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
                 if (sub == 0) {
                     if (dm.validate && !isfinite(vt)) bad |= 0x4u;
                     if (a.o) a.o[(tok_of(t) * Hv + h) * kD + drow] = o;
-                    Uout[(size_t)t * kUSub] = us;
+                    const int2 rp = recpos(t);
+                    const size_t bh = (size_t)rp.x * Hv + h;
+                    static_cast<UT *>(a.p.U)[((bh * (kD / kUSub) + tile) * dm.bt + rp.y) * kUSub + row] = us;
                     if (dm.keep_raw) {
-                        static_cast<InT *>(a.p.V)[(((size_t)r * Hv + h) * T + j0 + t) * kD + drow] =
-                            v_s[t * TPC * 32 + wt * 32 + row];
-                        if (tile == 0 && row == 0) a.p.B[((size_t)r * Hv + h) * T + j0 + t] = bt;
+                        static_cast<InT *>(a.p.V)[(bh * dm.bt + rp.y) * kD + drow] = v_s[t * TPC * 32 + wt * 32 + row];
+                        if (tile == 0 && row == 0) a.p.B[bh * dm.bt + rp.y] = bt;
                     }
                 }
             }
@@ -689,18 +717,27 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
             fence_proxy_async_smem();
             __syncthreads();
             if (tid == 0) {
-                bulk_s2g(a.p.state + (((size_t)r * Hv + h) * kD + (size_t)tile0 * 32) * kD, S_s, TPC * 32 * kD * 4);
+                bulk_s2g(a.p.state + ((sb * Hv + h) * kD + (size_t)tile0 * 32) * kD, S_s, TPC * 32 * kD * 4);
                 bulk_commit();
             }
         }
     }
     // ---- 4. records: k_t once per QK head, G_t per V head (first tile group)
     if (tg == 0) {
+        auto recpos = [&](int t) -> int2 {
+            if (!a.p.btab) return make_int2(r, j0 + t);
+            return make_int2(__ldcg(a.p.btab + (size_t)r * dm.maxb + (j0 + t) / dm.bt), (j0 + t) % dm.bt);
+        };
         if (h % dm.g == 0) {
-            InT *Kdst = static_cast<InT *>(a.p.K) + (((size_t)r * Hk + hk) * T + j0) * kD;
-            for (int idx = tid; idx < n_new * kD; idx += NTHR) Kdst[idx] = k_s[idx];
+            for (int idx = tid; idx < n_new * kD; idx += NTHR) {
+                const int2 rp = recpos(idx / kD);
+                static_cast<InT *>(a.p.K)[(((size_t)rp.x * Hk + hk) * dm.bt + rp.y) * kD + idx % kD] = k_s[idx];
+            }
         }
-        if (tid < n_new) a.p.G[((size_t)r * Hv + h) * T + j0 + tid] = Gn_s[tid];
+        if (tid < n_new) {
+            const int2 rp = recpos(tid);
+            a.p.G[((size_t)rp.x * Hv + h) * dm.bt + rp.y] = Gn_s[tid];
+        }
     }
     if (a.kind != CK_VERIFY && tid == 0 && ticket == (int)(gridDim.x * gridDim.y) - 1) {
         a.p.ticket[r] = 0;

@@ -72,10 +72,10 @@ template <typename InT, typename UT, bool FP32_IN, int kFoldNJ, int KCM, bool RA
 __global__ void __launch_bounds__(kFoldThreads, RAW ? 4 : (kFoldNJ == 128 ? 2 : (kFoldNJ == 32 && KCM == 16 ? 8 : 4))) fold_kernel(const FoldArgs a) {
     constexpr int NPAR = kFoldThreads / kFoldNJ;   // token parities per B row
     const int jh = blockIdx.x, h = blockIdx.y, zi = blockIdx.z;
-    const int r = a.first + zi;
+    const int r = a.slots ? __ldcg(a.slots + zi) : a.first + zi;
     const int tid = threadIdx.x, warp = tid >> 5;
     const Dims dm = a.dm;
-    const int T = dm.T, Hv = dm.Hv;
+    const int Hv = dm.Hv, bt = dm.bt;
     const int hk = h / dm.g;
     const int KC = a.kc;                           // staging chunk (multiple of 8, <= 32)
 
@@ -87,17 +87,29 @@ __global__ void __launch_bounds__(kFoldThreads, RAW ? 4 : (kFoldNJ == 128 ? 2 : 
     uint64_t *bar_mma = bar_ld + 1;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bar_ld + 2);
     int *meta = reinterpret_cast<int *>(bar_ld + 3);      // n, zero_s0
-    float *state_tile = a.p.state + (((size_t)r * Hv + h) * kD + (size_t)jh * kFoldNJ) * kD;
+    const size_t sb = a.p.sidx ? (size_t)__ldcg(a.p.sidx + r) : (size_t)r;
+    float *state_tile = a.p.state + ((sb * Hv + h) * kD + (size_t)jh * kFoldNJ) * kD;
 
-    const InT *Kb = static_cast<const InT *>(a.p.K) + ((size_t)r * dm.Hk + hk) * T * kD;
-    // U is tile-major [R][Hv][d/kUSub][T][kUSub]
-    const UT *Ub = static_cast<const UT *>(a.p.U) + ((size_t)r * Hv + h) * T * kD;
-    const float *Gb = a.p.G + ((size_t)r * Hv + h) * T;
     // per-thread operand coordinates: A column c = tid (all KC tokens);
     // B row j = tid % NJ, tokens i = ip (mod NPAR)
     const int c = tid, jb = tid % kFoldNJ, ip = tid / kFoldNJ;
     const int jr = jh * kFoldNJ + jb;
-    const UT *Urow = Ub + (size_t)(jr / kUSub) * T * kUSub + jr % kUSub;
+    // record i of the slot (block table or the slot's own region): key row,
+    // this thread's delta value u_i[jr] (U is tile-major
+    // [blk][Hv][d/kUSub][bt][kUSub]), log decay, raw value, beta
+    auto rec = [&](int i) -> size_t {   // (block * Hv + h) * bt + offset
+        const int2 ba = rec_at(dm, a.p, r, i);
+        return ((size_t)ba.x * Hv + h) * bt + ba.y;
+    };
+    auto Kp = [&](int i) {
+        const int2 ba = rec_at(dm, a.p, r, i);
+        return static_cast<const InT *>(a.p.K) + (((size_t)ba.x * dm.Hk + hk) * bt + ba.y) * kD;
+    };
+    auto Up = [&](int i) {
+        const int2 ba = rec_at(dm, a.p, r, i);
+        return static_cast<const UT *>(a.p.U) +
+               ((((size_t)ba.x * Hv + h) * (kD / kUSub) + jr / kUSub) * bt + ba.y) * kUSub + jr % kUSub;
+    };
     // operands of one chunk: K^T column c, u_i[j], G_i — the first chunk is
     // requested at entry, bounded by the host's record count (in-capacity
     // reads past a slot's own count are never used)
@@ -108,7 +120,7 @@ __global__ void __launch_bounds__(kFoldThreads, RAW ? 4 : (kFoldNJ == 128 ? 2 : 
             if constexpr (RAW)
                 kv[i] = (i < kn) ? reinterpret_cast<const float *>(smem + L.Ks)[(kc0 + i) * kD + c] : 0.f;
             else
-                kv[i] = (i < kn) ? to_f(Kb[(size_t)(kc0 + i) * kD + c]) : 0.f;
+                kv[i] = (i < kn) ? to_f(Kp(kc0 + i)[c]) : 0.f;
         }
 #pragma unroll
         for (int q = 0; q < KCM / NPAR; ++q) {
@@ -116,11 +128,11 @@ __global__ void __launch_bounds__(kFoldThreads, RAW ? 4 : (kFoldNJ == 128 ? 2 : 
             if constexpr (RAW)
                 uv[q] = (i < kn) ? reinterpret_cast<const float *>(smem + L.Us)[(kc0 + i) * kFoldNJ + jb] : 0.f;
             else
-                uv[q] = (i < kn) ? to_f(Urow[(size_t)(kc0 + i) * kUSub]) : 0.f;
+                uv[q] = (i < kn) ? to_f(*Up(kc0 + i)) : 0.f;
             if constexpr (RAW)
                 gv[q] = (i < kn) ? reinterpret_cast<const float *>(smem + L.Gs)[kc0 + i] : 0.f;
             else
-                gv[q] = (i < kn) ? Gb[kc0 + i] : 0.f;
+                gv[q] = (i < kn) ? a.p.G[rec(kc0 + i)] : 0.f;
         }
     };
 
@@ -170,12 +182,10 @@ __global__ void __launch_bounds__(kFoldThreads, RAW ? 4 : (kFoldNJ == 128 ? 2 : 
         float *Gs = reinterpret_cast<float *>(smem + L.Gs);
         float *Bs = reinterpret_cast<float *>(smem + L.Bs);
         float *Us = reinterpret_cast<float *>(smem + L.Us);
-        const InT *Vb = static_cast<const InT *>(a.p.V) + ((size_t)r * Hv + h) * T * kD;
-        const float *Bb = a.p.B + ((size_t)r * Hv + h) * T;
         for (int i0 = 0; i0 < a.kcap; i0 += 16) {
             float t[16];
 #pragma unroll
-            for (int u = 0; u < 16; ++u) t[u] = (i0 + u < a.kcap) ? to_f(Kb[(size_t)(i0 + u) * kD + c]) : 0.f;
+            for (int u = 0; u < 16; ++u) t[u] = (i0 + u < a.kcap) ? to_f(Kp(i0 + u)[c]) : 0.f;
 #pragma unroll
             for (int u = 0; u < 16; ++u) Ks[(i0 + u) * kD + c] = t[u];
         }
@@ -184,12 +194,12 @@ __global__ void __launch_bounds__(kFoldThreads, RAW ? 4 : (kFoldNJ == 128 ? 2 : 
 #pragma unroll
             for (int u = 0; u < 16; ++u) {
                 const int i = i0 + NPAR * u;
-                t[u] = (i < a.kcap) ? to_f(Vb[(size_t)i * kD + jr]) : 0.f;
+                t[u] = (i < a.kcap) ? to_f(static_cast<const InT *>(a.p.V)[rec(i) * kD + jr]) : 0.f;
             }
 #pragma unroll
             for (int u = 0; u < 16; ++u) if (i0 + NPAR * u < a.kcap) Us[(i0 + NPAR * u) * kFoldNJ + jb] = t[u];
         }
-        for (int i = tid; i < a.kcap; i += kFoldThreads) { Gs[i] = Gb[i]; Bs[i] = Bb[i]; }
+        for (int i = tid; i < a.kcap; i += kFoldThreads) { Gs[i] = a.p.G[rec(i)]; Bs[i] = a.p.B[rec(i)]; }
     } else {
         load_chunk(0, min(KC, a.kcap));
     }
@@ -305,7 +315,7 @@ __global__ void __launch_bounds__(kFoldThreads, RAW ? 4 : (kFoldNJ == 128 ? 2 : 
         __syncthreads();
         load_chunk(0, min(KC, n));
     }
-    const float g_last = Gb[n - 1];
+    const float g_last = a.p.G[rec(n - 1)];
     const uint32_t idesc = idesc_tf32(128, kFoldNJ);
     uint32_t mma_phase = 0;
 

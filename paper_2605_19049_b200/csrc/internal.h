@@ -16,9 +16,18 @@ inline int max_new_per_launch(int /*g*/) { return kMaxNewPerLaunch; }
 
 enum DType : int { DT_F32 = 0, DT_BF16 = 1, DT_F16 = 2 };
 
+// Record addressing.  Records live in blocks of `bt` token positions:
+// K [nblk][Hk][bt][d], U [nblk][Hv][d/kUSub][bt][kUSub], G [nblk][Hv][bt],
+// V [nblk][Hv][bt][d], B [nblk][Hv][bt].  Contiguous handles (block_tokens =
+// 0) are the special case bt = T, one block per slot, block id = slot, no
+// table; paged handles look position p of slot r up in the block table:
+// block btab[r * maxb + p / bt], offset p % bt.
+// States: slot r's state is state[sidx[r]] with a state pool, state[r]
+// without (sidx == nullptr).
 struct Dims {
     int R, Hk, Hv, g, T, C;
     int in_dt, u_dt, keep_raw, validate;
+    int bt, maxb;        // tokens per record block; blocks per slot (table row length)
 };
 
 // Launch overlap (la_set_overlap, programmatic dependent launch): pdl = the
@@ -37,7 +46,18 @@ struct Ptrs {
     float *B;                // [R][Hv][T]        (keep_raw)
     int *occ, *len, *mode, *ticket;
     unsigned *status;
+    const int *sidx;         // [R] state index per slot, or nullptr (identity)
+    const int *btab;         // [R][maxb] record block table, or nullptr (contiguous)
 };
+
+#ifdef __CUDACC__
+__device__ __forceinline__ size_t state_of(const Ptrs &p, int r) { return p.sidx ? (size_t)p.sidx[r] : (size_t)r; }
+// (block id, offset) of record position pos of slot r
+__device__ __forceinline__ int2 rec_at(const Dims &dm, const Ptrs &p, int r, int pos) {
+    if (!p.btab) return make_int2(r, pos);
+    return make_int2(p.btab[(size_t)r * dm.maxb + pos / dm.bt], pos % dm.bt);
+}
+#endif
 
 // What the chunk-attend kernel does with the counters and the state.
 enum ChunkKind : int {
@@ -60,6 +80,8 @@ struct ChunkArgs {
     const void *q, *k, *v;
     const float *alpha, *beta;
     float *o;           // may be null (prefill without outputs)
+    const int *slots = nullptr;   // index-array batch: slot of CTA row zi (else first + zi)
+    const int *pos = nullptr;     // ... and its row in the caller's inputs / outputs (else zi)
     int dry = 0;        // 1: check the launch configuration only, enqueue nothing
     int pdl = 0, pdl_early = 0;   // see Ptrs/launch overlap below
     int fold = 0;                 // decode: fold a slot's buffer in the step that fills it
@@ -85,6 +107,7 @@ struct FoldArgs {
     int kc;             // staging chunk (set by launch_fold)
     int raw = 0;        // mode ii: recompute u from the raw records (keep_raw) by the UT transform
     int pdl = 0, pdl_early = 0;
+    const int *slots = nullptr;   // index-array batch (else first + zi)
 };
 
 struct RecArgs {
@@ -106,6 +129,16 @@ cudaError_t launch_fold(const FoldArgs &a, cudaStream_t s, int64_t *launches);
 cudaError_t launch_recurrent_step(const RecArgs &a, cudaStream_t s, int64_t *launches);
 cudaError_t launch_recurrent_verify(const RecArgs &a, cudaStream_t s, int64_t *launches);
 cudaError_t launch_recurrent_commit(const RecArgs &a, cudaStream_t s, int64_t *launches);
+// Writes dst[idx[i]] = val[i] for the staged host entries (block tables,
+// state indices, work lists): small host decisions delivered in stream order
+// as kernel parameters (no host buffer outlives the call; graph-capturable).
+constexpr int kStageMax = 3000;
+struct StageArgs {
+    int *dst;
+    int n;
+    int2 e[kStageMax];   // (index, value)
+};
+cudaError_t launch_stage(const StageArgs &a, cudaStream_t s, int64_t *launches);
 cudaError_t launch_reset(const Dims &dm, const Ptrs &p, int first, int n, int mode, int zero_state,
                          cudaStream_t s, int64_t *launches);
 

@@ -46,6 +46,11 @@ size_t round_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 size_t dt_size(int dt) { return dt == LA_DT_F32 ? 4 : 2; }
 
 constexpr size_t kAlign = 1024;
+// work lists of an index-array batch (la_decode_mixed): chunkwise slots and
+// their input rows, direct slots and their input rows, slots to flush, slots
+// to compress
+constexpr int kWorkLists = 6;
+enum { WL_CW = 0, WL_CW_POS = 1, WL_DR = 2, WL_DR_POS = 3, WL_FL = 4, WL_CP = 5 };
 
 }  // namespace
 
@@ -58,6 +63,15 @@ struct la_buf {
     Ptrs p;
     int device;
     std::vector<int32_t> occ, len, mode, pending;   // host mirror
+    // pools: record blocks per slot, state index per slot
+    // (-1: none); LIFO free stacks, back() = next id (initially ascending)
+    bool paged = false, state_pool = false;
+    std::vector<std::vector<int32_t>> blocks;
+    std::vector<int32_t> sidx;
+    std::vector<int32_t> free_blocks, free_states;
+    int *meta_i = nullptr;                           // device meta as int32
+    std::vector<int32_t> wl_dev;                     // what the device work lists hold (-1: unknown)
+    size_t i_sidx = 0, i_btab = 0, i_wl = 0;         // int32 offsets in meta
     int64_t launches = 0;
     int overlap = 0;                                 // la_set_overlap
     int auto_flush = 0;                              // la_set_auto_flush
@@ -88,8 +102,9 @@ PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
 const void *state_tmap(la_buf *b) {
     if (b->tmap_state == 0) {
         b->tmap_state = 2;
+        if (b->sz.n_states <= 0) return nullptr;
         if (auto enc = tmap_encoder()) {
-            const cuuint64_t dims[2] = {(cuuint64_t)kD, (cuuint64_t)b->dm.R * b->dm.Hv * kD};
+            const cuuint64_t dims[2] = {(cuuint64_t)kD, (cuuint64_t)b->sz.n_states * b->dm.Hv * kD};
             const cuuint64_t strides[1] = {(cuuint64_t)kD * 4};
             const cuuint32_t box[2] = {32, 128};
             const cuuint32_t estr[2] = {1, 1};
@@ -150,6 +165,10 @@ la_status check_config(const la_config *c) {
     if (c->u_dtype == LA_DT_F16 && c->in_dtype != LA_DT_BF16) return fail(LA_ERR_UNSUPPORTED, "u_dtype F16 requires in_dtype BF16");
     if (c->keep_raw != 0 && c->keep_raw != 1) return fail(LA_ERR_INVALID, "keep_raw must be 0 or 1");
     if (c->validate != 0 && c->validate != 1) return fail(LA_ERR_INVALID, "validate must be 0 or 1");
+    if (c->block_tokens != 0 && (c->block_tokens < 4 || c->block_tokens > 128 || c->block_tokens % 4))
+        return fail(LA_ERR_INVALID, "block_tokens must be 0 or a multiple of 4 in [4, 128]");
+    if (c->block_tokens != 0 && c->n_blocks < 1) return fail(LA_ERR_INVALID, "a paged handle needs n_blocks >= 1");
+    if (c->state_slots < -1) return fail(LA_ERR_INVALID, "state_slots must be >= -1");
     return LA_OK;
 }
 
@@ -161,17 +180,30 @@ void compute_sizes(const la_config *c, la_sizes *s) {
     const int T = (std::max(c->chunk + c->max_drafts, c->short_cap) + 3) & ~3;
     s->capacity = T;
     s->align = kAlign;
-    s->state_bytes = R * Hv * d * d * 4;
+    // record blocks: one per slot of T records, or a pool of n_blocks blocks
+    const size_t bt = c->block_tokens ? c->block_tokens : T;
+    const size_t nb = c->block_tokens ? c->n_blocks : R;
+    s->block_tokens = (int32_t)bt;
+    s->n_blocks = (int32_t)nb;
+    s->max_blocks = (int32_t)((T + bt - 1) / bt);
+    s->n_states = c->state_slots == 0 ? c->max_slots : std::max(c->state_slots, 0);
+    s->state_bytes = (size_t)s->n_states * Hv * d * d * 4;
     size_t o = 0;
-    s->off_k = o; o = round_up(o + R * Hk * T * d * dt_size(c->in_dtype), kAlign);
-    s->off_u = o; o = round_up(o + R * Hv * T * d * dt_size(c->u_dtype), kAlign);
-    s->off_g = o; o = round_up(o + R * Hv * T * 4, kAlign);
+    s->off_k = o; o = round_up(o + nb * Hk * bt * d * dt_size(c->in_dtype), kAlign);
+    s->off_u = o; o = round_up(o + nb * Hv * bt * d * dt_size(c->u_dtype), kAlign);
+    s->off_g = o; o = round_up(o + nb * Hv * bt * 4, kAlign);
     if (c->keep_raw) {
-        s->off_v = o; o = round_up(o + R * Hv * T * d * dt_size(c->in_dtype), kAlign);
-        s->off_b = o; o = round_up(o + R * Hv * T * 4, kAlign);
+        s->off_v = o; o = round_up(o + nb * Hv * bt * d * dt_size(c->in_dtype), kAlign);
+        s->off_b = o; o = round_up(o + nb * Hv * bt * 4, kAlign);
     }
     s->buffer_bytes = o;
-    s->meta_bytes = round_up(4 * R * 4 + 16, 256);
+    // meta: occ, len, mode, ticket [R], status; state index [R]; block table
+    // [R][max_blocks]; work lists [kWorkLists][R]
+    size_t m = 4 * R * 4 + 16;
+    s->off_sidx = m; m += R * 4;
+    s->off_btab = m; m += R * (size_t)s->max_blocks * 4;
+    s->off_wl = m;   m += kWorkLists * R * 4;
+    s->meta_bytes = round_up(m, 256);
     s->record_bytes = Hk * d * dt_size(c->in_dtype) + Hv * d * dt_size(c->u_dtype) + Hv * 4 +
                       (c->keep_raw ? Hv * d * dt_size(c->in_dtype) + Hv * 4 : 0);
 }
@@ -186,6 +218,12 @@ la_status check_handle(la_buf *b) {
 la_status check_range(la_buf *b, int32_t first, int32_t n) {
     if (first < 0 || n < 0 || (int64_t)first + n > b->cfg.max_slots)
         return fail(LA_ERR_INVALID, "slot range [%d, %d) outside [0, %d)", first, first + n, b->cfg.max_slots);
+    return LA_OK;
+}
+
+la_status check_chunkwise(la_buf *b, int r) {
+    if (b->mode[r] != LA_MODE_CHUNKWISE) return fail(LA_ERR_MODE, "slot %d is not CHUNKWISE", r);
+    if (b->sidx[r] < 0) return fail(LA_ERR_MODE, "slot %d holds no state (reset it as CHUNKWISE)", r);
     return LA_OK;
 }
 
@@ -217,14 +255,17 @@ la_status set_device(la_buf *b) {
 // advanced for decode/direct/prefill, an explicit offset (j_add) for verify.
 cudaError_t run_chunk(la_buf *b, int first, int n, int n_tok, int j0_cap, int tok_base, int tok_total,
                       int kind, const void *q, const void *k, const void *v, const float *alpha,
-                      const float *beta, float *o, cudaStream_t s, int fold = 0) {
+                      const float *beta, float *o, cudaStream_t s, int fold = 0,
+                      const int *slots = nullptr, const int *pos = nullptr, int passes = 3) {
     const int mx = max_new_per_launch(b->dm.g);
     const size_t isz = dt_size(b->cfg.in_dtype);
     const size_t d = kD;
     // pass 0 checks every launch configuration (shared memory, grid) without
     // enqueueing anything, so a configuration error leaves the handle and the
-    // device untouched (all-or-nothing); pass 1 enqueues
+    // device untouched (all-or-nothing); pass 1 enqueues.  Index-array
+    // batches (slots/pos: device work lists) address the inputs by row.
     for (int pass = 0; pass < 2; ++pass) {
+        if (!(passes & (1 << pass))) continue;
         for (int off = 0; off < n_tok; off += mx) {
             const int m = std::min(mx, n_tok - off);
             for (int s0 = 0; s0 < n; s0 += kMaxSlotsPerLaunch) {
@@ -234,17 +275,20 @@ cudaError_t run_chunk(la_buf *b, int first, int n, int n_tok, int j0_cap, int to
                 a.n_new = m; a.j0_cap = j0_cap + off;
                 a.j_add = (kind == CK_VERIFY) ? off : 0;
                 a.tok_total = tok_total; a.tok_offset = tok_base + off; a.kind = kind;
-                const size_t sq = (size_t)s0 * tok_total;          // token rows skipped
+                const size_t sq = slots ? 0 : (size_t)s0 * tok_total;          // token rows skipped
                 a.q = static_cast<const char *>(q) + sq * b->dm.Hk * d * isz;
                 a.k = static_cast<const char *>(k) + sq * b->dm.Hk * d * isz;
                 a.v = static_cast<const char *>(v) + sq * b->dm.Hv * d * isz;
                 a.alpha = alpha + sq * b->dm.Hv;
                 a.beta = beta + sq * b->dm.Hv;
                 a.o = o ? o + sq * b->dm.Hv * d : nullptr;
+                a.slots = slots ? slots + s0 : nullptr;
+                a.pos = pos ? pos + s0 : nullptr;
                 a.tmap = (kind == CK_VERIFY || kind == CK_PREFILL) && m >= 2 ? state_tmap(b) : nullptr;
                 a.fold = fold;
                 a.dry = pass == 0;
                 overlap_flags(b, s, a);
+                if (slots) a.pdl_early = 0;   // the slot list itself comes from a previous grid
                 cudaError_t e = launch_chunk(a, s, &b->launches);
                 if (e != cudaSuccess) return e;
                 if (pass == 1) note_launch(b, s, fold != 0);
@@ -255,15 +299,17 @@ cudaError_t run_chunk(la_buf *b, int first, int n, int n_tok, int j0_cap, int to
 }
 
 // Folds (flush, commit, compression) in slot batches of kMaxSlotsPerLaunch
-// (the slot index is a grid dimension).
+// (the slot index is a grid dimension), over a range or a device slot list.
 cudaError_t run_fold(la_buf *b, FoldArgs a, cudaStream_t s) {
     const int first = a.first, n = a.n;
-    const int *nacc = a.nacc;
+    const int *nacc = a.nacc, *slots = a.slots;
     for (int s0 = 0; s0 < n; s0 += kMaxSlotsPerLaunch) {
         a.first = first + s0;
         a.n = std::min(kMaxSlotsPerLaunch, n - s0);
         a.nacc = nacc ? nacc + s0 : nullptr;
+        a.slots = slots ? slots + s0 : nullptr;
         overlap_flags(b, s, a);
+        if (slots) a.pdl_early = 0;
         cudaError_t e = launch_fold(a, s, &b->launches);
         if (e != cudaSuccess) return e;
         note_launch(b, s, true);
@@ -299,6 +345,103 @@ cudaError_t run_rec(la_buf *b, RecArgs a, cudaStream_t s, bool wrote, Launch lau
         note_launch(b, s, wrote);
     }
     return cudaSuccess;
+}
+
+// ---------------------------------------------------------------- pools
+// Host decisions (which block / state a slot gets) are made here and
+// delivered to the device in stream order by the staging kernel: (meta int32
+// index, value) entries passed as kernel parameters.
+struct Stage {
+    std::vector<int2> e;
+    void put(size_t idx, int v) { e.push_back(make_int2((int)idx, v)); }
+};
+
+int blocks_for(const la_buf *b, int npos) { return b->paged ? (npos + b->dm.bt - 1) / b->dm.bt : 0; }
+
+// Grow the slots' block lists to cover their record positions [0, npos):
+// check (ok == nullptr: take) -- the check happens before anything mutates
+struct Grow { int slot, npos; };
+la_status check_blocks(la_buf *b, const std::vector<Grow> &g) {
+    if (!b->paged) return LA_OK;
+    size_t need = 0;
+    for (const Grow &x : g) need += (size_t)std::max(0, blocks_for(b, x.npos) - (int)b->blocks[x.slot].size());
+    if (need > b->free_blocks.size())
+        return fail(LA_ERR_CAPACITY, "record block pool exhausted: %zu blocks needed, %zu free", need,
+                    b->free_blocks.size());
+    return LA_OK;
+}
+void take_blocks(la_buf *b, const std::vector<Grow> &g, Stage &st) {
+    if (!b->paged) return;
+    for (const Grow &x : g) {
+        std::vector<int32_t> &bl = b->blocks[x.slot];
+        while ((int)bl.size() < blocks_for(b, x.npos)) {
+            const int id = b->free_blocks.back();
+            b->free_blocks.pop_back();
+            st.put(b->i_btab + (size_t)x.slot * b->dm.maxb + bl.size(), id);
+            bl.push_back(id);
+        }
+    }
+}
+// return the slot's blocks beyond the first `keep` to the pool (LIFO)
+void drop_blocks(la_buf *b, int r, int keep) {
+    std::vector<int32_t> &bl = b->blocks[r];
+    while ((int)bl.size() > keep) {
+        b->free_blocks.push_back(bl.back());
+        bl.pop_back();
+    }
+}
+la_status check_states(la_buf *b, size_t need) {
+    if (need == 0) return LA_OK;
+    if (!b->state_pool || b->sz.n_states == 0) return fail(LA_ERR_CAPACITY, "the handle has no states (state_slots = -1)");
+    if (need > b->free_states.size())
+        return fail(LA_ERR_CAPACITY, "state pool exhausted: %zu states needed, %zu free", need, b->free_states.size());
+    return LA_OK;
+}
+void take_state(la_buf *b, int r, Stage &st) {
+    if (b->sidx[r] >= 0) return;
+    const int id = b->free_states.back();
+    b->free_states.pop_back();
+    b->sidx[r] = id;
+    st.put(b->i_sidx + r, id);
+}
+void drop_state(la_buf *b, int r) {
+    if (!b->state_pool || b->sidx[r] < 0) return;
+    b->free_states.push_back(b->sidx[r]);
+    b->sidx[r] = -1;
+}
+cudaError_t run_stage(la_buf *b, Stage &st, cudaStream_t s) {
+    for (size_t o = 0; o < st.e.size(); o += kStageMax) {
+        StageArgs a;
+        a.dst = b->meta_i;
+        a.n = (int)std::min(st.e.size() - o, (size_t)kStageMax);
+        memcpy(a.e, st.e.data() + o, a.n * sizeof(int2));
+        cudaError_t e = launch_stage(a, s, &b->launches);
+        if (e != cudaSuccess) return e;
+        note_launch(b, s, true);   // state indices / tables moved: no early state loads next
+    }
+    st.e.clear();
+    return cudaSuccess;
+}
+// stage work list `w` (only entries that differ from what the device holds)
+void stage_list(la_buf *b, int w, const std::vector<int> &vals, Stage &st) {
+    const size_t R = b->cfg.max_slots;
+    for (size_t j = 0; j < vals.size(); ++j) {
+        int32_t &dev = b->wl_dev[w * R + j];
+        if (dev != vals[j]) {
+            st.put(b->i_wl + w * R + j, vals[j]);
+            dev = vals[j];
+        }
+    }
+}
+const int *wl_ptr(const la_buf *b, int w) { return b->meta_i + b->i_wl + (size_t)w * b->cfg.max_slots; }
+
+// range -> Grow list of the slots' positions [0, base[r] + add)
+std::vector<Grow> grow_range(la_buf *b, int first, int n, const std::vector<int32_t> &base, int add) {
+    std::vector<Grow> g;
+    if (!b->paged) return g;
+    g.reserve(n);
+    for (int r = first; r < first + n; ++r) g.push_back({r, base[r] + add});
+    return g;
 }
 
 }  // namespace
@@ -344,6 +487,21 @@ la_status la_buf_create(const la_config *cfg, void *state, void *buffer, void *m
     p.occ = m; p.len = m + R; p.mode = m + 2 * R; p.ticket = m + 3 * R;
     p.status = reinterpret_cast<unsigned *>(m + 4 * R);
     b->occ.assign(R, 0); b->len.assign(R, 0); b->mode.assign(R, 0); b->pending.assign(R, 0);
+    dm.bt = b->sz.block_tokens; dm.maxb = b->sz.max_blocks;
+    b->meta_i = m;
+    b->i_sidx = b->sz.off_sidx / 4; b->i_btab = b->sz.off_btab / 4; b->i_wl = b->sz.off_wl / 4;
+    b->paged = cfg->block_tokens != 0;
+    b->state_pool = cfg->state_slots != 0;
+    p.sidx = b->state_pool ? m + b->i_sidx : nullptr;
+    p.btab = b->paged ? m + b->i_btab : nullptr;
+    b->blocks.assign(R, {});
+    // without a state pool slot r owns state r; with one, slots start empty
+    b->sidx.assign(R, -1);
+    if (!b->state_pool)
+        for (int r = 0; r < R; ++r) b->sidx[r] = r;
+    b->wl_dev.assign((size_t)kWorkLists * R, -1);
+    for (int i = b->sz.n_blocks - 1; b->paged && i >= 0; --i) b->free_blocks.push_back(i);
+    for (int i = b->sz.n_states - 1; b->state_pool && i >= 0; --i) b->free_states.push_back(i);
     *out = b;
     return LA_OK;
 }
@@ -354,30 +512,56 @@ la_status la_buf_destroy(la_buf *buf) {
     return LA_OK;
 }
 
-la_status la_request_reset(la_buf *b, int32_t first, int32_t n, int32_t mode, int32_t zero_state,
-                           la_stream stream) {
+static la_status reset_impl(la_buf *b, int32_t first, int32_t n, int32_t mode, int32_t zero_state,
+                            la_stream stream, bool release) {
     la_status st;
     if ((st = check_handle(b)) != LA_OK || (st = check_range(b, first, n)) != LA_OK) return st;
     if (mode != LA_MODE_CHUNKWISE && mode != LA_MODE_DIRECT) return fail(LA_ERR_INVALID, "bad mode");
-    if (mode == LA_MODE_DIRECT && b->cfg.short_cap == 0) return fail(LA_ERR_MODE, "direct mode disabled (short_cap = 0)");
+    if (!release && mode == LA_MODE_DIRECT && b->cfg.short_cap == 0)
+        return fail(LA_ERR_MODE, "direct mode disabled (short_cap = 0)");
     if (n == 0) return LA_OK;
+    // state pool: CHUNKWISE slots keep or take a state, DIRECT slots return theirs
+    size_t need = 0;
+    if (b->state_pool && mode == LA_MODE_CHUNKWISE)
+        for (int r = first; r < first + n; ++r) need += b->sidx[r] < 0;
+    if ((st = check_states(b, need)) != LA_OK) return st;
     if ((st = set_device(b)) != LA_OK) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
     std::lock_guard<std::mutex> lk(g_enqueue_mu);
+    Stage stg;
+    for (int r = first; r < first + n; ++r) {
+        drop_blocks(b, r, 0);                     // the buffer empties: blocks back to the pool
+        if (mode == LA_MODE_DIRECT) drop_state(b, r);
+        else take_state(b, r, stg);
+    }
+    cudaError_t e = run_stage(b, stg, s);
+    if (e != cudaSuccess) return cuda_fail(e, "stage launch");
+    // zeroing a state needs one: DIRECT slots of a state pool hold none
+    const int zero = zero_state && !(b->state_pool && mode == LA_MODE_DIRECT) ? 1 : 0;
     for (int s0 = 0; s0 < n; s0 += kMaxSlotsPerLaunch) {
-        cudaError_t e = launch_reset(b->dm, b->p, first + s0, std::min(kMaxSlotsPerLaunch, n - s0), mode,
-                                     zero_state ? 1 : 0, static_cast<cudaStream_t>(stream), &b->launches);
+        e = launch_reset(b->dm, b->p, first + s0, std::min(kMaxSlotsPerLaunch, n - s0), mode, zero, s,
+                         &b->launches);
         if (e != cudaSuccess) return cuda_fail(e, "reset launch");
-        note_launch(b, static_cast<cudaStream_t>(stream), zero_state != 0);
+        note_launch(b, s, zero != 0);
     }
     // status word: cleared by a reset covering slot 0
-    if (first == 0) {
-        cudaError_t e = cudaMemsetAsync(b->p.status, 0, sizeof(unsigned), static_cast<cudaStream_t>(stream));
+    if (first == 0 && !release) {
+        e = cudaMemsetAsync(b->p.status, 0, sizeof(unsigned), s);
         if (e != cudaSuccess) return cuda_fail(e, "status clear");
     }
     for (int r = first; r < first + n; ++r) {
         b->occ[r] = 0; b->len[r] = 0; b->mode[r] = mode; b->pending[r] = 0;
     }
     return LA_OK;
+}
+
+la_status la_request_reset(la_buf *b, int32_t first, int32_t n, int32_t mode, int32_t zero_state,
+                           la_stream stream) {
+    return reset_impl(b, first, n, mode, zero_state, stream, false);
+}
+
+la_status la_request_release(la_buf *b, int32_t first, int32_t n, la_stream stream) {
+    return reset_impl(b, first, n, LA_MODE_DIRECT, 0, stream, true);
 }
 
 la_status la_decode_step(la_buf *b, int32_t first, int32_t n, const void *q, const void *k,
@@ -389,7 +573,7 @@ la_status la_decode_step(la_buf *b, int32_t first, int32_t n, const void *q, con
     int j0_cap = 0;
     bool fills = false;
     for (int r = first; r < first + n; ++r) {
-        if (b->mode[r] != LA_MODE_CHUNKWISE) return fail(LA_ERR_MODE, "slot %d is not CHUNKWISE", r);
+        if ((st = check_chunkwise(b, r)) != LA_OK) return st;
         if (b->pending[r]) return fail(LA_ERR_MODE, "slot %d has a pending verify (commit first)", r);
         if (b->occ[r] >= b->cfg.chunk) return fail(LA_ERR_CAPACITY, "slot %d buffer full (call la_flush)", r);
         j0_cap = std::max(j0_cap, b->occ[r]);
@@ -398,9 +582,17 @@ la_status la_decode_step(la_buf *b, int32_t first, int32_t n, const void *q, con
     if (n == 0) return LA_OK;
     if ((st = set_device(b)) != LA_OK) return st;
     const int fold = (b->auto_flush && fills && b->cfg.chunk <= 32) ? 1 : 0;
+    const std::vector<Grow> g = grow_range(b, first, n, b->occ, 1);
+    if ((st = check_blocks(b, g)) != LA_OK) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
     std::lock_guard<std::mutex> lk(g_enqueue_mu);
-    cudaError_t e = run_chunk(b, first, n, 1, j0_cap, 0, 1, CK_DECODE, q, k, v, alpha, beta, o,
-                              static_cast<cudaStream_t>(stream), fold);
+    cudaError_t e = run_chunk(b, first, n, 1, j0_cap, 0, 1, CK_DECODE, q, k, v, alpha, beta, o, s, fold,
+                              nullptr, nullptr, 1);
+    if (e != cudaSuccess) return cuda_fail(e, "decode launch configuration");
+    Stage stg;
+    take_blocks(b, g, stg);
+    if ((e = run_stage(b, stg, s)) != cudaSuccess) return cuda_fail(e, "stage launch");
+    e = run_chunk(b, first, n, 1, j0_cap, 0, 1, CK_DECODE, q, k, v, alpha, beta, o, s, fold, nullptr, nullptr, 2);
     if (e != cudaSuccess) return cuda_fail(e, "decode launch");
     for (int r = first; r < first + n; ++r) {
         b->occ[r] += 1;
@@ -430,13 +622,28 @@ la_status la_flush(la_buf *b, int32_t first, int32_t n, int32_t kind, la_stream 
         kcap = std::max(kcap, nr);
     }
     if (!any) return LA_OK;   // empty flush is not an error (SPEC flush_and_free)
+    // compression of DIRECT slots (FORCE): each needs a state from the pool
+    size_t need = 0;
+    if (kind == LA_FLUSH_FORCE)
+        for (int r = first; r < first + n; ++r) need += b->mode[r] == LA_MODE_DIRECT && b->len[r] > 0 && b->sidx[r] < 0;
+    if ((st = check_states(b, need)) != LA_OK) return st;
+    for (int r = first; r < first + n; ++r)
+        if (b->mode[r] == LA_MODE_CHUNKWISE && b->sidx[r] < 0 && b->occ[r] > 0)
+            return fail(LA_ERR_MODE, "slot %d holds no state", r);
     if ((st = set_device(b)) != LA_OK) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
     FoldArgs a;
     a.dm = b->dm; a.p = b->p; a.first = first; a.n = n;
     a.kind = kind == LA_FLUSH_FULL ? FK_FULL : FK_FORCE; a.nacc = nullptr; a.n_draft = 0; a.kcap = kcap; a.spec = all;
     a.raw = raw ? 1 : 0;
     std::lock_guard<std::mutex> lk(g_enqueue_mu);
-    cudaError_t e = run_fold(b, a, static_cast<cudaStream_t>(stream));
+    Stage stg;
+    if (kind == LA_FLUSH_FORCE)
+        for (int r = first; r < first + n; ++r)
+            if (b->mode[r] == LA_MODE_DIRECT && b->len[r] > 0) take_state(b, r, stg);
+    cudaError_t e = run_stage(b, stg, s);
+    if (e != cudaSuccess) return cuda_fail(e, "stage launch");
+    e = run_fold(b, a, s);
     if (e != cudaSuccess) return cuda_fail(e, "flush launch");
     for (int r = first; r < first + n; ++r) {
         if (kind == LA_FLUSH_FULL) {
@@ -445,6 +652,8 @@ la_status la_flush(la_buf *b, int32_t first, int32_t n, int32_t kind, la_stream 
             b->occ[r] = 0;
         } else if (b->len[r] > 0) {
             b->mode[r] = LA_MODE_CHUNKWISE; b->len[r] = 0; b->occ[r] = 0;
+            // the compressed records are dead: keep the blocks a chunkwise buffer uses
+            drop_blocks(b, r, blocks_for(b, b->cfg.chunk + b->cfg.max_drafts));
         }
     }
     return LA_OK;
@@ -460,16 +669,25 @@ la_status la_verify_drafts(la_buf *b, int32_t first, int32_t n, int32_t n_draft,
         return fail(LA_ERR_INVALID, "n_draft %d outside [1, %d]", n_draft, b->cfg.max_drafts);
     int j0_cap = 0;
     for (int r = first; r < first + n; ++r) {
-        if (b->mode[r] != LA_MODE_CHUNKWISE) return fail(LA_ERR_MODE, "slot %d is not CHUNKWISE", r);
+        if ((st = check_chunkwise(b, r)) != LA_OK) return st;
         if (b->pending[r]) return fail(LA_ERR_MODE, "slot %d already has a pending verify", r);
         if (b->occ[r] + n_draft > b->sz.capacity) return fail(LA_ERR_CAPACITY, "slot %d: occ + n_draft > capacity", r);
         j0_cap = std::max(j0_cap, b->occ[r]);
     }
     if (n == 0) return LA_OK;
     if ((st = set_device(b)) != LA_OK) return st;
+    const std::vector<Grow> g = grow_range(b, first, n, b->occ, n_draft);
+    if ((st = check_blocks(b, g)) != LA_OK) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
     std::lock_guard<std::mutex> lk(g_enqueue_mu);
-    cudaError_t e = run_chunk(b, first, n, n_draft, j0_cap, 0, n_draft, CK_VERIFY, q, k, v, alpha, beta, o,
-                              static_cast<cudaStream_t>(stream));
+    cudaError_t e = run_chunk(b, first, n, n_draft, j0_cap, 0, n_draft, CK_VERIFY, q, k, v, alpha, beta, o, s, 0,
+                              nullptr, nullptr, 1);
+    if (e != cudaSuccess) return cuda_fail(e, "verify launch configuration");
+    Stage stg;
+    take_blocks(b, g, stg);
+    if ((e = run_stage(b, stg, s)) != cudaSuccess) return cuda_fail(e, "stage launch");
+    e = run_chunk(b, first, n, n_draft, j0_cap, 0, n_draft, CK_VERIFY, q, k, v, alpha, beta, o, s, 0,
+                  nullptr, nullptr, 2);
     if (e != cudaSuccess) return cuda_fail(e, "verify launch");
     for (int r = first; r < first + n; ++r) b->pending[r] = n_draft;
     return LA_OK;
@@ -513,9 +731,17 @@ la_status la_direct_short(la_buf *b, int32_t first, int32_t n, int32_t n_new, co
     }
     if (n == 0) return LA_OK;
     if ((st = set_device(b)) != LA_OK) return st;
+    const std::vector<Grow> g = grow_range(b, first, n, b->len, n_new);
+    if ((st = check_blocks(b, g)) != LA_OK) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
     std::lock_guard<std::mutex> lk(g_enqueue_mu);
-    cudaError_t e = run_chunk(b, first, n, n_new, j0_cap, 0, n_new, CK_DIRECT, q, k, v, alpha, beta, o,
-                              static_cast<cudaStream_t>(stream));
+    cudaError_t e = run_chunk(b, first, n, n_new, j0_cap, 0, n_new, CK_DIRECT, q, k, v, alpha, beta, o, s, 0,
+                              nullptr, nullptr, 1);
+    if (e != cudaSuccess) return cuda_fail(e, "direct launch configuration");
+    Stage stg;
+    take_blocks(b, g, stg);
+    if ((e = run_stage(b, stg, s)) != cudaSuccess) return cuda_fail(e, "stage launch");
+    e = run_chunk(b, first, n, n_new, j0_cap, 0, n_new, CK_DIRECT, q, k, v, alpha, beta, o, s, 0, nullptr, nullptr, 2);
     if (e != cudaSuccess) return cuda_fail(e, "direct launch");
     for (int r = first; r < first + n; ++r) b->len[r] += n_new;
     return LA_OK;
@@ -528,7 +754,7 @@ la_status la_prefill(la_buf *b, int32_t first, int32_t n, int32_t n_tok, const v
     if ((st = check_inputs(q, k, v, alpha, beta, o, false)) != LA_OK) return st;
     if (n_tok < 0) return fail(LA_ERR_INVALID, "n_tok must be >= 0");
     for (int r = first; r < first + n; ++r) {
-        if (b->mode[r] != LA_MODE_CHUNKWISE) return fail(LA_ERR_MODE, "slot %d is not CHUNKWISE", r);
+        if ((st = check_chunkwise(b, r)) != LA_OK) return st;
         if (b->pending[r]) return fail(LA_ERR_MODE, "slot %d has a pending verify", r);
         if (b->occ[r] != 0) return fail(LA_ERR_MODE, "slot %d: prefill needs an empty buffer (occ = %d)", r, b->occ[r]);
     }
@@ -536,7 +762,15 @@ la_status la_prefill(la_buf *b, int32_t first, int32_t n, int32_t n_tok, const v
     if ((st = set_device(b)) != LA_OK) return st;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const int C = b->cfg.chunk;
+    const std::vector<Grow> g = grow_range(b, first, n, b->occ, std::min(C, n_tok));
+    if ((st = check_blocks(b, g)) != LA_OK) return st;
     std::lock_guard<std::mutex> lk(g_enqueue_mu);
+    {
+        Stage stg;
+        take_blocks(b, g, stg);
+        cudaError_t e = run_stage(b, stg, s);
+        if (e != cudaSuccess) return cuda_fail(e, "stage launch");
+    }
     for (int c0 = 0; c0 < n_tok; c0 += C) {
         const int cn = std::min(C, n_tok - c0);
         cudaError_t e = run_chunk(b, first, n, cn, 0, c0, n_tok, CK_PREFILL, q, k, v, alpha, beta, o, s);
@@ -557,7 +791,7 @@ la_status la_recurrent_step(la_buf *b, int32_t first, int32_t n, const void *q, 
     if ((st = check_handle(b)) != LA_OK || (st = check_range(b, first, n)) != LA_OK) return st;
     if ((st = check_inputs(q, k, v, alpha, beta, o, true)) != LA_OK) return st;
     for (int r = first; r < first + n; ++r)
-        if (b->mode[r] != LA_MODE_CHUNKWISE || b->occ[r] != 0 || b->pending[r])
+        if (b->mode[r] != LA_MODE_CHUNKWISE || b->sidx[r] < 0 || b->occ[r] != 0 || b->pending[r])
             return fail(LA_ERR_MODE, "slot %d: recurrent step needs a CHUNKWISE slot with an empty buffer", r);
     if (n == 0) return LA_OK;
     if ((st = set_device(b)) != LA_OK) return st;
@@ -579,7 +813,7 @@ la_status la_recurrent_verify(la_buf *b, int32_t first, int32_t n, int32_t n_dra
     if (!temp || !aligned(temp, 16)) return fail(LA_ERR_INVALID, "temp must be a 16-byte aligned device pointer");
     if (n_draft < 1 || n_draft > kMaxNewPerLaunch) return fail(LA_ERR_INVALID, "n_draft outside [1, 16]");
     for (int r = first; r < first + n; ++r)
-        if (b->mode[r] != LA_MODE_CHUNKWISE || b->occ[r] != 0 || b->pending[r])
+        if (b->mode[r] != LA_MODE_CHUNKWISE || b->sidx[r] < 0 || b->occ[r] != 0 || b->pending[r])
             return fail(LA_ERR_MODE, "slot %d: recurrent verify needs a CHUNKWISE slot with an empty buffer", r);
     if (n == 0) return LA_OK;
     if ((st = set_device(b)) != LA_OK) return st;
@@ -599,7 +833,7 @@ la_status la_recurrent_commit(la_buf *b, int32_t first, int32_t n, int32_t n_dra
     if (!n_accepted || !temp || !aligned(temp, 16)) return fail(LA_ERR_INVALID, "null/misaligned pointer");
     if (n_draft < 1 || n_draft > kMaxNewPerLaunch) return fail(LA_ERR_INVALID, "n_draft outside [1, 16]");
     for (int r = first; r < first + n; ++r)
-        if (b->mode[r] != LA_MODE_CHUNKWISE || b->occ[r] != 0 || b->pending[r])
+        if (b->mode[r] != LA_MODE_CHUNKWISE || b->sidx[r] < 0 || b->occ[r] != 0 || b->pending[r])
             return fail(LA_ERR_MODE, "slot %d: recurrent commit needs a CHUNKWISE slot with an empty buffer", r);
     if (n == 0) return LA_OK;
     if ((st = set_device(b)) != LA_OK) return st;
@@ -609,6 +843,129 @@ la_status la_recurrent_commit(la_buf *b, int32_t first, int32_t n, int32_t n_dra
     std::lock_guard<std::mutex> lk(g_enqueue_mu);
     cudaError_t e = run_rec(b, a, static_cast<cudaStream_t>(stream), true, launch_recurrent_commit);
     if (e != cudaSuccess) return cuda_fail(e, "recurrent commit launch");
+    return LA_OK;
+}
+
+la_status la_decode_mixed(la_buf *b, int32_t n, const int32_t *slots, const void *q, const void *k,
+                          const void *v, const float *alpha, const float *beta, float *o, la_stream stream) {
+    la_status st;
+    if ((st = check_handle(b)) != LA_OK) return st;
+    const int R = b->cfg.max_slots, C = b->cfg.chunk;
+    if (n < 0 || n > R) return fail(LA_ERR_INVALID, "n %d outside [0, max_slots]", n);
+    if (n == 0) return LA_OK;
+    if (!slots) return fail(LA_ERR_INVALID, "null slots");
+    if ((st = check_inputs(q, k, v, alpha, beta, o, true)) != LA_OK) return st;
+    // route every slot to its form (host mirror): chunkwise decode (+ eager
+    // flush of a buffer it fills), KV-only decode, or compression at
+    // len == short_cap followed by chunkwise decode
+    std::vector<int> cw, cw_pos, dr, dr_pos, fl, cp;
+    std::vector<char> seen(R, 0);
+    std::vector<Grow> g;
+    int j0_cw = 0, j0_dr = 0, cp_cap = 0;
+    size_t need_states = 0;
+    for (int i = 0; i < n; ++i) {
+        const int r = slots[i];
+        if (r < 0 || r >= R) return fail(LA_ERR_INVALID, "slots[%d] = %d outside [0, %d)", i, r, R);
+        if (seen[r]) return fail(LA_ERR_INVALID, "slot %d appears twice in the batch", r);
+        seen[r] = 1;
+        if (b->pending[r]) return fail(LA_ERR_MODE, "slot %d has a pending verify (commit first)", r);
+        if (b->mode[r] == LA_MODE_CHUNKWISE) {
+            if (b->sidx[r] < 0) return fail(LA_ERR_MODE, "slot %d holds no state (reset it as CHUNKWISE)", r);
+            if (b->occ[r] >= C) return fail(LA_ERR_CAPACITY, "slot %d buffer full (call la_flush)", r);
+            j0_cw = std::max(j0_cw, b->occ[r]);
+            g.push_back({r, b->occ[r] + 1});
+            if (b->occ[r] + 1 == C) fl.push_back(r);
+            cw.push_back(r); cw_pos.push_back(i);
+        } else if (b->len[r] < b->cfg.short_cap) {
+            j0_dr = std::max(j0_dr, b->len[r]);
+            g.push_back({r, b->len[r] + 1});
+            dr.push_back(r); dr_pos.push_back(i);
+        } else {
+            cp.push_back(r);
+            cp_cap = std::max(cp_cap, b->len[r]);
+            need_states += b->sidx[r] < 0;
+            g.push_back({r, 1});
+            if (C == 1) fl.push_back(r);
+            cw.push_back(r); cw_pos.push_back(i);
+        }
+    }
+    if ((st = check_states(b, need_states)) != LA_OK) return st;
+    // blocks: compressed slots keep what a chunkwise buffer uses, the rest return first
+    size_t freed = 0;
+    const int keep = blocks_for(b, C + b->cfg.max_drafts);
+    for (int r : cp) freed += (size_t)std::max(0, (int)b->blocks[r].size() - std::max(keep, 1));
+    {
+        size_t need = 0;
+        for (const Grow &x : g) need += (size_t)std::max(0, blocks_for(b, x.npos) - (int)b->blocks[x.slot].size());
+        if (b->paged && need > b->free_blocks.size() + freed)
+            return fail(LA_ERR_CAPACITY, "record block pool exhausted: %zu blocks needed, %zu free", need,
+                        b->free_blocks.size() + freed);
+    }
+    if ((st = set_device(b)) != LA_OK) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    std::lock_guard<std::mutex> lk(g_enqueue_mu);
+    // launch configurations first (all-or-nothing)
+    const int *W_CW = wl_ptr(b, WL_CW), *W_CWP = wl_ptr(b, WL_CW_POS), *W_DR = wl_ptr(b, WL_DR),
+              *W_DRP = wl_ptr(b, WL_DR_POS), *W_FL = wl_ptr(b, WL_FL), *W_CP = wl_ptr(b, WL_CP);
+    cudaError_t e = cudaSuccess;
+    if (!cw.empty())
+        e = run_chunk(b, 0, (int)cw.size(), 1, j0_cw, 0, 1, CK_DECODE, q, k, v, alpha, beta, o, s, 0, W_CW, W_CWP, 1);
+    if (e == cudaSuccess && !dr.empty())
+        e = run_chunk(b, 0, (int)dr.size(), 1, j0_dr, 0, 1, CK_DIRECT, q, k, v, alpha, beta, o, s, 0, W_DR, W_DRP, 1);
+    if (e != cudaSuccess) return cuda_fail(e, "mixed decode launch configuration");
+    // pools and work lists -> one staging pass
+    Stage stg;
+    for (int r : cp) {
+        take_state(b, r, stg);
+        drop_blocks(b, r, std::max(keep, 1));
+    }
+    take_blocks(b, g, stg);
+    stage_list(b, WL_CW, cw, stg);
+    stage_list(b, WL_CW_POS, cw_pos, stg);
+    stage_list(b, WL_DR, dr, stg);
+    stage_list(b, WL_DR_POS, dr_pos, stg);
+    stage_list(b, WL_FL, fl, stg);
+    stage_list(b, WL_CP, cp, stg);
+    if ((e = run_stage(b, stg, s)) != cudaSuccess) return cuda_fail(e, "stage launch");
+    if (!cp.empty()) {   // compression: fold the len records into a zero state, mode -> CHUNKWISE
+        FoldArgs a;
+        a.dm = b->dm; a.p = b->p; a.first = 0; a.n = (int)cp.size(); a.slots = W_CP;
+        a.kind = FK_FORCE; a.nacc = nullptr; a.n_draft = 0; a.kcap = cp_cap; a.spec = 0;
+        if ((e = run_fold(b, a, s)) != cudaSuccess) return cuda_fail(e, "compression launch");
+    }
+    if (!cw.empty() &&
+        (e = run_chunk(b, 0, (int)cw.size(), 1, j0_cw, 0, 1, CK_DECODE, q, k, v, alpha, beta, o, s, 0, W_CW, W_CWP,
+                       2)) != cudaSuccess)
+        return cuda_fail(e, "mixed decode launch");
+    if (!dr.empty() &&
+        (e = run_chunk(b, 0, (int)dr.size(), 1, j0_dr, 0, 1, CK_DIRECT, q, k, v, alpha, beta, o, s, 0, W_DR, W_DRP,
+                       2)) != cudaSuccess)
+        return cuda_fail(e, "mixed direct launch");
+    if (!fl.empty()) {   // eager flush of the buffers this step filled (Z15)
+        FoldArgs a;
+        a.dm = b->dm; a.p = b->p; a.first = 0; a.n = (int)fl.size(); a.slots = W_FL;
+        a.kind = FK_FULL; a.nacc = nullptr; a.n_draft = 0; a.kcap = C; a.spec = 1;
+        if ((e = run_fold(b, a, s)) != cudaSuccess) return cuda_fail(e, "flush launch");
+    }
+    for (int r : cp) { b->mode[r] = LA_MODE_CHUNKWISE; b->len[r] = 0; b->occ[r] = 0; }
+    for (int r : cw) b->occ[r] = (b->occ[r] + 1 == C) ? 0 : b->occ[r] + 1;
+    for (int r : dr) b->len[r] += 1;
+    return LA_OK;
+}
+
+la_status la_pool_info(la_buf *b, int32_t *free_blocks, int32_t *total_blocks, int32_t *free_states,
+                       int32_t *total_states, int32_t slot, int32_t *slot_blocks, int32_t *slot_state) {
+    la_status st;
+    if ((st = check_handle(b)) != LA_OK) return st;
+    if (slot >= 0 && (st = check_range(b, slot, 1)) != LA_OK) return st;
+    if (free_blocks) *free_blocks = b->paged ? (int32_t)b->free_blocks.size() : 0;
+    if (total_blocks) *total_blocks = b->paged ? b->sz.n_blocks : 0;
+    if (free_states) *free_states = b->state_pool ? (int32_t)b->free_states.size() : 0;
+    if (total_states) *total_states = b->sz.n_states;
+    if (slot >= 0) {
+        if (slot_blocks) *slot_blocks = b->paged ? (int32_t)b->blocks[slot].size() : 1;
+        if (slot_state) *slot_state = b->sidx[slot];
+    }
     return LA_OK;
 }
 
@@ -632,9 +989,10 @@ la_status la_state_get(la_buf *b, int32_t slot, float *dst, la_stream stream) {
     la_status st;
     if ((st = check_handle(b)) != LA_OK || (st = check_range(b, slot, 1)) != LA_OK) return st;
     if (!dst) return fail(LA_ERR_INVALID, "null dst");
+    if (b->sidx[slot] < 0) return fail(LA_ERR_MODE, "slot %d holds no state", slot);
     if ((st = set_device(b)) != LA_OK) return st;
     const size_t bytes = (size_t)b->dm.Hv * kD * kD * 4;
-    cudaError_t e = cudaMemcpyAsync(dst, b->p.state + (size_t)slot * b->dm.Hv * kD * kD, bytes,
+    cudaError_t e = cudaMemcpyAsync(dst, b->p.state + (size_t)b->sidx[slot] * b->dm.Hv * kD * kD, bytes,
                                     cudaMemcpyDeviceToDevice, static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(e, "state_get copy");
     return LA_OK;
@@ -644,12 +1002,12 @@ la_status la_state_set(la_buf *b, int32_t slot, const float *src, la_stream stre
     la_status st;
     if ((st = check_handle(b)) != LA_OK || (st = check_range(b, slot, 1)) != LA_OK) return st;
     if (!src) return fail(LA_ERR_INVALID, "null src");
-    if (b->mode[slot] != LA_MODE_CHUNKWISE || b->occ[slot] != 0 || b->pending[slot])
+    if (b->mode[slot] != LA_MODE_CHUNKWISE || b->sidx[slot] < 0 || b->occ[slot] != 0 || b->pending[slot])
         return fail(LA_ERR_MODE, "slot %d: state_set needs a CHUNKWISE slot with an empty buffer", slot);
     if ((st = set_device(b)) != LA_OK) return st;
     std::lock_guard<std::mutex> lk(g_enqueue_mu);
     const size_t bytes = (size_t)b->dm.Hv * kD * kD * 4;
-    cudaError_t e = cudaMemcpyAsync(b->p.state + (size_t)slot * b->dm.Hv * kD * kD, src, bytes,
+    cudaError_t e = cudaMemcpyAsync(b->p.state + (size_t)b->sidx[slot] * b->dm.Hv * kD * kD, src, bytes,
                                     cudaMemcpyDeviceToDevice, static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(e, "state_set copy");
     note_launch(b, static_cast<cudaStream_t>(stream), true);

@@ -12,6 +12,10 @@
 
 namespace labuf {
 
+__device__ __forceinline__ size_t sidx_of(const Ptrs &p, int r) {
+    return p.sidx ? (size_t)__ldcg(p.sidx + r) : (size_t)r;
+}
+
 // ------------------------------------------------------------------ (5a)
 // CTA = (d_v tile of kRows rows, QK head, slot) over the g V heads of the
 // QK head.  Reads the state tile once, writes it once.
@@ -36,7 +40,7 @@ __global__ void __launch_bounds__(256) recurrent_step_kernel(const RecArgs a) {
     float *tiles[G];
 #pragma unroll
     for (int hh = 0; hh < G; ++hh)
-        tiles[hh] = a.p.state + (((size_t)r * Hv + hk * G + hh) * kD + (size_t)tile * ROWS) * kD;
+        tiles[hh] = a.p.state + ((sidx_of(a.p, r) * Hv + hk * G + hh) * kD + (size_t)tile * ROWS) * kD;
     if (tid == 0) {
         mbar_init(bar, 1);
         fence_mbar_init();
@@ -135,7 +139,7 @@ __global__ void __launch_bounds__(128) recurrent_verify_kernel(const RecArgs a) 
     float *be_s = al_s + 16;
     float *kqd = be_s + 16;                                          // k_t . q_t
 
-    const float *src = a.p.state + (((size_t)r * Hv + h) * kD + (size_t)tile * ROWS) * kD;
+    const float *src = a.p.state + ((sidx_of(a.p, r) * Hv + h) * kD + (size_t)tile * ROWS) * kD;
     const uint32_t bytes = ROWS * kD * 4 + (uint32_t)N * (2 * kD + ROWS) * isz;
     if (tid == 0) {
         mbar_init(bar, 1);
@@ -234,7 +238,7 @@ __global__ void __launch_bounds__(256) recurrent_commit_kernel(const RecArgs a) 
     if (na == 0) return;
     const float4 *src = reinterpret_cast<const float4 *>(
         a.temp + (((size_t)zi * a.n_draft + na - 1) * a.dm.Hv + h) * kD * kD);
-    float4 *dst = reinterpret_cast<float4 *>(a.p.state + ((size_t)r * a.dm.Hv + h) * kD * kD);
+    float4 *dst = reinterpret_cast<float4 *>(a.p.state + (sidx_of(a.p, r) * a.dm.Hv + h) * kD * kD);
     const int per = kD * kD / 4 / gridDim.x;
     const int base = blockIdx.x * per;
     for (int i = threadIdx.x; i < per; i += 256) dst[base + i] = src[base + i];
@@ -289,11 +293,26 @@ cudaError_t launch_recurrent_commit(const RecArgs &a, cudaStream_t s, int64_t *l
     return e;
 }
 
+// ------------------------------------------------------------------ stage
+__global__ void stage_kernel(const __grid_constant__ StageArgs a) {
+    if (a.n > 0) pdl_wait();   // the previous grid may still read the entries being replaced
+    pdl_trigger();
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += gridDim.x * blockDim.x)
+        a.dst[a.e[i].x] = a.e[i].y;
+}
+
+cudaError_t launch_stage(const StageArgs &a, cudaStream_t s, int64_t *launches) {
+    if (a.n <= 0) return cudaSuccess;
+    cudaError_t e = launch_k(stage_kernel, dim3((a.n + 255) / 256), dim3(256), 0, s, true, a);
+    if (e == cudaSuccess) ++*launches;
+    return e;
+}
+
 // ------------------------------------------------------------------ reset
 __global__ void reset_kernel(Ptrs p, Dims dm, int first, int n, int mode, int zero_state) {
     const int zi = blockIdx.y, r = first + zi;
     if (zero_state) {
-        float4 *st = reinterpret_cast<float4 *>(p.state + (size_t)r * dm.Hv * kD * kD);
+        float4 *st = reinterpret_cast<float4 *>(p.state + sidx_of(p, r) * dm.Hv * kD * kD);
         const size_t total = (size_t)dm.Hv * kD * kD / 4;
         for (size_t i = blockIdx.x * 256 + threadIdx.x; i < total; i += (size_t)gridDim.x * 256)
             st[i] = make_float4(0.f, 0.f, 0.f, 0.f);

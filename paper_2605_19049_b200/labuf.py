@@ -28,7 +28,8 @@ _STATUS_NAMES = {0: "LA_OK", 1: "LA_ERR_INVALID", 2: "LA_ERR_UNSUPPORTED", 3: "L
 
 # The exported entry points of include/la.h, in declaration order.
 EXPORTS = (
-    "la_buf_query", "la_buf_create", "la_buf_destroy", "la_request_reset", "la_decode_step",
+    "la_buf_query", "la_buf_create", "la_buf_destroy", "la_request_reset", "la_request_release",
+    "la_decode_mixed", "la_pool_info", "la_decode_step",
     "la_flush", "la_verify_drafts", "la_commit_accepted", "la_direct_short", "la_prefill",
     "la_recurrent_step", "la_recurrent_verify", "la_recurrent_commit", "la_set_overlap", "la_set_auto_flush",
     "la_state_get", "la_state_set", "la_slot_info", "la_device_status", "la_kernel_launches", "la_last_error",
@@ -45,7 +46,8 @@ class LaError(RuntimeError):
 class LaConfig(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int32) for n in (
         "max_slots", "n_qk_heads", "n_v_heads", "d_k", "d_v", "chunk", "max_drafts",
-        "short_cap", "in_dtype", "u_dtype", "keep_raw", "validate")]
+        "short_cap", "in_dtype", "u_dtype", "keep_raw", "validate", "block_tokens", "n_blocks",
+        "state_slots")]
 
 
 class LaSizes(ctypes.Structure):
@@ -54,7 +56,9 @@ class LaSizes(ctypes.Structure):
                 ("capacity", ctypes.c_int32), ("off_k", ctypes.c_size_t),
                 ("off_u", ctypes.c_size_t), ("off_g", ctypes.c_size_t),
                 ("off_v", ctypes.c_size_t), ("off_b", ctypes.c_size_t),
-                ("record_bytes", ctypes.c_size_t)]
+                ("record_bytes", ctypes.c_size_t), ("block_tokens", ctypes.c_int32),
+                ("n_blocks", ctypes.c_int32), ("max_blocks", ctypes.c_int32), ("n_states", ctypes.c_int32),
+                ("off_sidx", ctypes.c_size_t), ("off_btab", ctypes.c_size_t), ("off_wl", ctypes.c_size_t)]
 
 
 _lib = None
@@ -86,6 +90,9 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "la_buf_create": [P(LaConfig), VP, VP, VP, I32, P(VP)],
         "la_buf_destroy": [VP],
         "la_request_reset": [VP, I32, I32, I32, I32, VP],
+        "la_request_release": [VP, I32, I32, VP],
+        "la_decode_mixed": [VP, I32, VP, VP, VP, VP, VP, VP, VP, VP],
+        "la_pool_info": [VP, P(I32), P(I32), P(I32), P(I32), I32, P(I32), P(I32)],
         "la_decode_step": [VP, I32, I32, VP, VP, VP, VP, VP, VP, VP],
         "la_flush": [VP, I32, I32, I32, VP],
         "la_verify_drafts": [VP, I32, I32, I32, VP, VP, VP, VP, VP, VP, VP],
@@ -124,10 +131,14 @@ def _check(st: int):
 
 
 def make_config(max_slots, n_qk_heads=16, n_v_heads=32, chunk=16, max_drafts=0, short_cap=0,
-                in_dtype="bf16", u_dtype="f32", keep_raw=False, validate=False, d=128) -> LaConfig:
+                in_dtype="bf16", u_dtype="f32", keep_raw=False, validate=False, d=128,
+                block_tokens=0, n_blocks=0, state_slots=0) -> LaConfig:
+    """block_tokens > 0: paged record blocks from a pool of n_blocks (P:140-144);
+    state_slots > 0: a pool of that many states, -1: none, 0: one per slot."""
     dt = {"f32": LA_DT_F32, "bf16": LA_DT_BF16, "f16": LA_DT_F16}
     return LaConfig(max_slots, n_qk_heads, n_v_heads, d, d, chunk, max_drafts, short_cap,
-                    dt[in_dtype], dt[u_dtype], int(keep_raw), int(validate))
+                    dt[in_dtype], dt[u_dtype], int(keep_raw), int(validate), int(block_tokens),
+                    int(n_blocks), int(state_slots))
 
 
 def query(cfg: LaConfig) -> LaSizes:
@@ -184,9 +195,10 @@ class LaBuf:
     # ------------------------------------------------------------ views
     @property
     def state(self) -> torch.Tensor:
-        """fp32 [R][Hv][d_v][d_k] view of the state pool (device)."""
+        """fp32 [S][Hv][d_v][d_k] view of the state pool (device); S = max_slots
+        (state r = slot r) unless the handle has a state pool."""
         c = self.cfg
-        return self._state.view(torch.float32).view(c.max_slots, c.n_v_heads, c.d_v, c.d_k)
+        return self._state.view(torch.float32).view(self.sizes.n_states, c.n_v_heads, c.d_v, c.d_k)
 
     @property
     def capacity(self) -> int:
@@ -195,17 +207,17 @@ class LaBuf:
     def records(self):
         """Views of the buffered records (K, U, G): for tests and debugging."""
         c, s = self.cfg, self.sizes
-        T = s.capacity
+        T, nb = s.block_tokens, s.n_blocks     # records per block, blocks (= slots when contiguous)
         udt = torch.float32 if c.u_dtype == LA_DT_F32 else torch.float16
         isz = 4 if c.in_dtype == LA_DT_F32 else 2
         usz = 4 if c.u_dtype == LA_DT_F32 else 2
-        nK = c.max_slots * c.n_qk_heads * T * c.d_k
-        nU = c.max_slots * c.n_v_heads * T * c.d_v
-        K = self._buffer[s.off_k:s.off_k + nK * isz].view(self.in_torch).view(c.max_slots, c.n_qk_heads, T, c.d_k)
-        # u records are tile-major: [R][Hv][d_v/32][T][32]
-        U = self._buffer[s.off_u:s.off_u + nU * usz].view(udt).view(c.max_slots, c.n_v_heads, c.d_v // 32, T, 32)
-        G = self._buffer[s.off_g:s.off_g + c.max_slots * c.n_v_heads * T * 4].view(torch.float32).view(
-            c.max_slots, c.n_v_heads, T)
+        nK = nb * c.n_qk_heads * T * c.d_k
+        nU = nb * c.n_v_heads * T * c.d_v
+        K = self._buffer[s.off_k:s.off_k + nK * isz].view(self.in_torch).view(nb, c.n_qk_heads, T, c.d_k)
+        # u records are tile-major: [blocks][Hv][d_v/32][bt][32]
+        U = self._buffer[s.off_u:s.off_u + nU * usz].view(udt).view(nb, c.n_v_heads, c.d_v // 32, T, 32)
+        G = self._buffer[s.off_g:s.off_g + nb * c.n_v_heads * T * 4].view(torch.float32).view(
+            nb, c.n_v_heads, T)
         return K, U, G
 
     def __del__(self):
@@ -246,6 +258,34 @@ class LaBuf:
                   beta.unsqueeze(1), o.unsqueeze(1))
         _check(self.lib.la_decode_step(self.h, first, n, _ptr(q), _ptr(k), _ptr(v), _ptr(alpha),
                                        _ptr(beta), _ptr(o), _stream()))
+
+    def release(self, first=0, n=None):
+        """Return slots' record blocks and states to the pools (la_request_release)."""
+        n = self.cfg.max_slots - first if n is None else n
+        _check(self.lib.la_request_release(self.h, first, n, _stream()))
+
+    def decode_mixed(self, slots, q, k, v, alpha, beta, o):
+        """One token per slot of an index-array batch in each slot's own form
+        (la_decode_mixed).  slots: host int sequence (numpy / list); tensors
+        q,k [n,Hk,d], v [n,Hv,d], alpha,beta [n,Hv], o [n,Hv,d] by batch row."""
+        import numpy as np
+        sl = np.ascontiguousarray(np.asarray(slots, dtype=np.int32))
+        n = int(sl.shape[0])
+        self._tok(n, 1, q.unsqueeze(1), k.unsqueeze(1), v.unsqueeze(1), alpha.unsqueeze(1),
+                  beta.unsqueeze(1), o.unsqueeze(1))
+        _check(self.lib.la_decode_mixed(self.h, n, sl.ctypes.data_as(ctypes.c_void_p), _ptr(q), _ptr(k),
+                                        _ptr(v), _ptr(alpha), _ptr(beta), _ptr(o), _stream()))
+
+    def pool_info(self, slot=-1):
+        """dict: free/total blocks and states; with slot >= 0 also its block count and state index."""
+        v = [ctypes.c_int32() for _ in range(6)]
+        _check(self.lib.la_pool_info(self.h, *(ctypes.byref(x) for x in v[:4]), slot, ctypes.byref(v[4]),
+                                     ctypes.byref(v[5])))
+        out = {"free_blocks": v[0].value, "total_blocks": v[1].value, "free_states": v[2].value,
+               "total_states": v[3].value}
+        if slot >= 0:
+            out["slot_blocks"], out["slot_state"] = v[4].value, v[5].value
+        return out
 
     def flush(self, first=0, n=None, kind=LA_FLUSH_FULL):
         n = self.cfg.max_slots - first if n is None else n

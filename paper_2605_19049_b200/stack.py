@@ -160,3 +160,91 @@ class GdnStack:
                 if b is not None:
                     tot += b.sizes.state_bytes + b.sizes.buffer_bytes + b.sizes.meta_bytes
         return tot
+
+
+@dataclass
+class MixedStack:
+    """Config 5 on ONE handle per layer: a paged record pool
+    (blocks of 16 tokens) and a state pool sized for the
+    long-context requests plus headroom for compressions, serving the mixed
+    batch with one la_decode_mixed call per layer per step -- long slots
+    decode chunkwise (eager flush), short slots KV-only, and a short slot
+    whose context reaches short_cap is compressed into a pool state.
+    Short requests hold no state at all, so the stack fits one B200 (the two-
+    handle layout above reserves a state per short slot too)."""
+    spec: StackSpec
+    device: torch.device
+    layers: list = field(default_factory=list)
+    state_headroom: int = 64
+    block_tokens: int = 16
+
+    def config(self):
+        s = self.spec
+        n = s.n_long + s.n_short
+        bt = self.block_tokens
+        blocks = s.n_long * -(-s.chunk // bt) + s.n_short * -(-s.short_cap // bt)
+        return L.make_config(n, s.n_qk_heads, s.n_v_heads, chunk=s.chunk, short_cap=s.short_cap,
+                             in_dtype=s.in_dtype, u_dtype="f16" if s.in_dtype == "bf16" else "f32",
+                             validate=False, block_tokens=bt, n_blocks=blocks,
+                             state_slots=s.n_long + self.state_headroom)
+
+    @classmethod
+    def create(cls, spec: StackSpec, device, state_headroom=64):
+        st = cls(spec, torch.device(device), state_headroom=state_headroom)
+        cfg = st.config()
+        st.layers = [L.LaBuf(cfg, device=st.device) for _ in range(spec.n_layers)]
+        return st
+
+    @staticmethod
+    def footprint_of(spec: StackSpec, state_headroom=64) -> int:
+        sz = L.query(MixedStack(spec, torch.device("cpu"), state_headroom=state_headroom).config())
+        return (sz.state_bytes + sz.buffer_bytes + sz.meta_bytes) * spec.n_layers
+
+    def footprint_bytes(self):
+        return sum(b.sizes.state_bytes + b.sizes.buffer_bytes + b.sizes.meta_bytes for b in self.layers)
+
+    def reset(self, states):
+        """states[l]: fp32 [n_long, Hv, d, d] start states of layer l's long slots
+        (slots 0..n_long-1; a fresh pool hands them states 0..n_long-1 in order)."""
+        s = self.spec
+        for b, S0 in zip(self.layers, states):
+            b.reset(0, s.n_long, mode=L.LA_MODE_CHUNKWISE, zero_state=False)
+            if s.n_short:
+                b.reset(s.n_long, s.n_short, mode=L.LA_MODE_DIRECT, zero_state=False)
+            assert b.pool_info(s.n_long - 1)["slot_state"] == s.n_long - 1
+            b.state[:s.n_long].copy_(S0)
+
+    def warmup(self, long_tok, short_tok):
+        """Ragged starting points as in GdnStack.warmup (long occupancies
+        staggered over 0..C-1, short contexts L0 per group); returns the
+        warm-up outputs for tests."""
+        outs = {}
+        s = self.spec
+        Hv, d = s.n_v_heads, 128
+        groups = long_groups(s)
+        for l, b in enumerate(self.layers):
+            for t in range(s.chunk - 1):
+                first = next((f for f, m, occ in groups if occ > t), None)
+                if first is None:
+                    break
+                x = long_tok(l, t)
+                idx = list(range(first, s.n_long))
+                o = torch.empty(len(idx), Hv, d, dtype=torch.float32, device=self.device)
+                b.decode_mixed(idx, *(x[k][first:].contiguous() for k in ("q", "k", "v", "alpha", "beta")), o)
+                outs[("long", l, t)] = (first, o)
+            for g, (first, m, l0) in enumerate(short_groups(s)):
+                x = short_tok(l, g)
+                o = torch.empty(m, l0, Hv, d, dtype=torch.float32, device=self.device)
+                b.direct_short(s.n_long + first, x["q"], x["k"], x["v"], x["alpha"], x["beta"], o)
+                outs[("short", l, g)] = (first, o)
+        return outs
+
+    def step(self, inputs, outputs, slots=None):
+        """One decode step of the stack: per layer ONE la_decode_mixed over the
+        batch (`slots`, default all, in slot order); inputs[l] / outputs[l]
+        are the layer's [n, ...] tensors by batch row."""
+        s = self.spec
+        if slots is None:
+            slots = range(s.n_long + s.n_short)
+        for b, x, o in zip(self.layers, inputs, outputs):
+            b.decode_mixed(slots, x["q"], x["k"], x["v"], x["alpha"], x["beta"], o)

@@ -205,3 +205,54 @@ def test_launch_options_and_raw_flag_validation(lib):
     assert lib.la_flush(h, 0, 8, L.LA_FLUSH_FULL | L.LA_FLUSH_RAW, None) == L.LA_OK
     assert lib.la_kernel_launches(h) == 0
     lib.la_buf_destroy(h)
+
+
+# ------------------------------------------------------------------ pools
+def test_paged_sizes_and_state_pool(lib):
+    """Paged handles size the buffer by the block pool (n_blocks x block_tokens
+    records), a state pool sizes the state by state_slots, and meta
+    carries the state index, block table and work lists (include/la.h)."""
+    R, Hk, Hv, d = 8, 16, 32, 128
+    s = L.query(_cfg(block_tokens=8, n_blocks=40, state_slots=5))
+    T = 64
+    assert (s.block_tokens, s.n_blocks, s.max_blocks, s.n_states) == (8, 40, T // 8, 5)
+    assert s.state_bytes == 5 * Hv * d * d * 4
+    assert s.off_u >= 40 * Hk * 8 * d * 2 and s.off_g >= s.off_u + 40 * Hv * 8 * d * 4
+    assert s.buffer_bytes >= s.off_g + 40 * Hv * 8 * 4
+    assert s.off_sidx == 4 * R * 4 + 16 and s.off_btab == s.off_sidx + R * 4
+    assert s.off_wl == s.off_btab + R * (T // 8) * 4 and s.meta_bytes >= s.off_wl + 6 * R * 4
+    c = L.query(_cfg())            # contiguous: one block of T records per slot, one state per slot
+    assert (c.block_tokens, c.n_blocks, c.max_blocks, c.n_states) == (T, R, 1, R)
+    assert L.query(_cfg(state_slots=-1)).state_bytes == 0     # KV-only handle
+
+
+@pytest.mark.parametrize("kw", [dict(block_tokens=6, n_blocks=4), dict(block_tokens=8, n_blocks=0),
+                                dict(block_tokens=132, n_blocks=4), dict(state_slots=-2)])
+def test_pool_config_rejections(lib, kw):
+    with pytest.raises(L.LaError) as e:
+        L.query(_cfg(**kw))
+    assert e.value.status == L.LA_ERR_INVALID
+
+
+def test_state_pool_exhaustion_before_device_work(lib):
+    """Without states (state_slots = -1) a slot cannot become CHUNKWISE, and a
+    slot that holds no state cannot decode: both rejected on the host, before
+    any CUDA call, pools and mirror unchanged."""
+    h = _fake_handle(lib, _cfg(block_tokens=8, n_blocks=16, state_slots=-1))
+    assert lib.la_request_reset(h, 0, 1, L.LA_MODE_CHUNKWISE, 0, None) == L.LA_ERR_CAPACITY
+    P = ctypes.c_void_p
+    ok = P(FAKE * 5)
+    assert lib.la_decode_step(h, 0, 1, ok, ok, ok, ok, ok, ok, None) == L.LA_ERR_MODE
+    sl = (ctypes.c_int32 * 2)(0, 0)
+    assert lib.la_decode_mixed(h, 2, sl, ok, ok, ok, ok, ok, ok, None) == L.LA_ERR_MODE      # no state
+    v = [ctypes.c_int32() for _ in range(6)]
+    assert lib.la_pool_info(h, *(ctypes.byref(x) for x in v[:4]), 0, ctypes.byref(v[4]), ctypes.byref(v[5])) == L.LA_OK
+    assert [x.value for x in v] == [16, 16, 0, 0, 0, -1]
+    assert lib.la_kernel_launches(h) == 0
+    lib.la_buf_destroy(h)
+    h = _fake_handle(lib, _cfg())      # contiguous: every slot owns its state
+    assert lib.la_decode_mixed(h, 2, sl, ok, ok, ok, ok, ok, ok, None) == L.LA_ERR_INVALID   # duplicate slot
+    sl[1] = 8
+    assert lib.la_decode_mixed(h, 2, sl, ok, ok, ok, ok, ok, ok, None) == L.LA_ERR_INVALID   # out of range
+    assert lib.la_kernel_launches(h) == 0
+    lib.la_buf_destroy(h)
