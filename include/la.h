@@ -107,6 +107,14 @@ typedef enum {
 } la_status;
 
 typedef enum { LA_DT_F32 = 0, LA_DT_BF16 = 1, LA_DT_F16 = 2 } la_dtype;
+/* Linear-attention variant of a handle (Table 1):
+ *   GDN     S_t = alpha_t S_{t-1} (I - beta_t k_t k_t^T) + beta_t v_t k_t^T
+ *   GATED   S_t = alpha_t S_{t-1} + v_t k_t^T   (scalar-gated LA, no delta rule;
+ *           beta ignored)
+ *   VANILLA S_t = S_{t-1} + v_t k_t^T           (alpha, beta ignored)
+ * The buffered value is u_t = v_t for the two delta-free variants; every
+ * kernel, the fold and the recurrent baselines honour the variant. */
+typedef enum { LA_VARIANT_GDN = 0, LA_VARIANT_GATED = 1, LA_VARIANT_VANILLA = 2 } la_variant;
 typedef enum { LA_MODE_CHUNKWISE = 0, LA_MODE_DIRECT = 1 } la_mode;
 typedef enum {
     LA_FLUSH_FULL = 0,   /* fold only slots whose buffer holds `chunk` records */
@@ -147,6 +155,7 @@ typedef struct {
     int32_t n_blocks;    /* paged: blocks in the pool (>= 1); else ignored    */
     int32_t state_slots; /* 0: one state per slot; > 0: a pool of that many
                             states, assigned on demand; -1: no states          */
+    int32_t variant;     /* la_variant (0 = GDN)                              */
 } la_config;
 
 typedef struct {
@@ -249,6 +258,29 @@ LA_API la_status la_verify_drafts(la_buf *buf, int32_t first, int32_t n, int32_t
  * same n_draft. */
 LA_API la_status la_commit_accepted(la_buf *buf, int32_t first, int32_t n,
                              const int32_t *n_accepted, la_stream stream);
+
+/* Multi-round buffered speculation: commit the accepted
+ * prefix by APPENDING it -- the accepted drafts' records (k, u, G) are
+ * already the recurrence's records (u_t depends only on tokens <= t),
+ * so the device occupancy advances by n_accepted[r] and nothing is folded.
+ * The state is folded only when the buffer could not take another round of
+ * max_drafts drafts (then exactly as la_commit_accepted: records
+ * [0, occ + n_accepted)).  The host mirror then holds an upper bound of the
+ * occupancy (it never reads n_accepted): until a fold, the slots accept only
+ * la_verify_drafts, commits and la_flush(FORCE) (LA_ERR_MODE otherwise).
+ * Same argument rules as la_commit_accepted. */
+LA_API la_status la_commit_append(la_buf *buf, int32_t first, int32_t n,
+                           const int32_t *n_accepted, la_stream stream);
+
+/* State rebuild / fork for KV-based prefix caching: the state of
+ * slot `dst` becomes the state slot `src` had after its first n_records
+ * buffered records: e^{G_{n-1}} S0 + sum_{i<n} e^{G_{n-1}-G_i} u_i k_i^T with
+ * S0 = src's state (CHUNKWISE src) or 0 (DIRECT src: the state rebuilt from
+ * the cached KVs alone).  src is not modified; dst must be a
+ * CHUNKWISE slot with an empty buffer (e.g. just reset), dst != src,
+ * 1 <= n_records <= src's buffered count. */
+LA_API la_status la_state_fork(la_buf *buf, int32_t src, int32_t dst, int32_t n_records,
+                        la_stream stream);
 
 /* Direct (KV-only) short-context decoding, kernel (4) (P:200-213,
  * P:374-378): for DIRECT slots, outputs of n_new new tokens computed only

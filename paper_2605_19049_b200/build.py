@@ -16,7 +16,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "liblabuf.so")
 
-CU_SOURCES = ["chunk.cu", "fold.cu", "recurrent.cu"]
+CU_SOURCES = ["chunk.cu", "chunk_f32_direct.cu", "chunk_f32_state.cu", "chunk_bf16_direct.cu",
+              "chunk_bf16_state.cu", "chunk_bf16h_direct.cu", "chunk_bf16h_state.cu", "fold.cu", "recurrent.cu"]
 CPP_SOURCES = ["la.cpp", "tp.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -26,7 +27,7 @@ def _sources():
 
 
 def _deps():
-    out = _sources() + [os.path.join(CSRC, f) for f in ("device.cuh", "internal.h")]
+    out = _sources() + [os.path.join(CSRC, f) for f in ("device.cuh", "internal.h", "chunk.cuh")]
     out.append(os.path.join(ROOT, "include", "la.h"))
     return out
 

@@ -1,813 +1,22 @@
-// chunk.cu — kernels (1) buffered decode, (3) parallel draft verification,
-// (4) direct short-context decoding, and the prefill chunk step.
-//
-// All compute, for n_new new tokens t of one request slot r and one V head
-// (QK head = h / g), against j0 buffered records (k_i, u_i, G_i):
-//
-//   G_t = G_{t-1} + ln alpha_t                  (cumulative log decay, reading Z2)
-//   a_t = S0 k_t,  b_t = S0 q_t                 (one read of the state tile; absent for direct)
-//   u_t = beta_t (v_t - e^{G_t} a_t - sum_{i<j0+t} e^{G_t-G_i} (k_t.k_i) u_i)
-//   o_t = e^{G_t} b_t + sum_{i<=j0+t} e^{G_t-G_i} (q_t.k_i) u_i
-//
-// which is the single-token chunkwise form P:403-406 (decode, subscripts per
-// readings Z2/Z3), the chunkwise matrix form P:392-399 solved by forward
-// substitution over the new tokens (verify, prefill: the UT transform of
-// P:395-397), and the parallel form P:374-386 with S0 = 0 (direct).
-// New records (k_t, u_t, G_t) are appended at position j0 + t.
-//
-// B200 structure (measured, tools/microbench_bulk.cu): HBM is saturated by
-// many small CTAs that each put their whole working set in flight with a
-// few bulk copies (cp.async.bulk -> SASS UBLKCP) on one mbarrier — 7.4 TB/s
-// even with 1 KB pieces — while a single issuing thread per SM cannot issue
-// small copies fast enough.  So: one CTA of TPC warps per (row-tile group,
-// V head, slot).  At entry its warps issue the copies — the TPC x 32 rows
-// of fp32 state of the head (ONE contiguous copy, 16 KiB per tile), the
-// tiles' u sub-tiles of all buffered records (contiguous by the tile-major U
-// layout), the QK head's key rows, the log decays and the new tokens — and
-// several CTAs per SM overlap one CTA's compute with the others' loads.
-// Compute: warp w owns d_v tile w (32 rows).  (A) Every state row and every
-// key row is reduced against k_t and q_t by 4-lane teams (8 rows per warp
-// step; each lane owns eight parity-swizzled 16-byte column chunks, so the
-// shared-memory reads are conflict-free; packed FFMA2 dot products; 2 shuffle
-// levels per value); the key rows are shared out over the CTA's warps.  One block
-// barrier.  (B) The forward substitution over the new tokens with one lane
-// per d_v row, and the o / u / record stores.
-#include <cuda.h>
-
-#include <cstdlib>
-
-#include "device.cuh"
-#include "internal.h"
+// chunk.cu — launch dispatch of the chunk-attend kernel (chunk.cuh): kernels
+// (1) buffered decode, (3) parallel draft verification, (4) direct
+// short-context decoding and the prefill chunk step, by input / delta-value
+// dtype and by kind (the instantiations live in chunk_<dtype>_<kind>.cu).
+#include "chunk.cuh"
 
 namespace labuf {
 
-constexpr int kChunkTPC = 2;        // d_v tiles (warps) per CTA for the state kinds
-constexpr int kDirectTPC = 4;       // ... and for direct slots (the key rows dominate)
-
-__host__ __device__ inline uint32_t al128(uint32_t x) { return (x + 127u) & ~127u; }
-
-struct CtaLayout {
-    uint32_t S, U, K, Gs, q, k, v, kq32, Ck, Cq, av, bv, Gn, Bn, Y, Kf, bar, bytes;
-};
-
-// tensor-core state pass: B operand rows (k_t, q_t of every new token, zero
-// padded to the MMA N granule of 16 at M = 128)
-__host__ __device__ constexpr int tc_nmma(int nt) { return (2 * nt + 15) / 16 * 16; }
-
-__host__ __device__ inline CtaLayout cta_layout(int TPC, int nt, bool has_state, int jcap, int isz, int usz,
-                                                bool tc = false, bool fold = false) {
-    CtaLayout L;
-    const int J = jcap + nt;
-    uint32_t o = 0;
-    // (tc: 1 KiB of slack so the 128-byte-swizzled state tile starts 1024-aligned)
-    L.S = o;  o = al128(o + (has_state ? (uint32_t)(TPC * 32 * kD * 4) + (tc ? 1024u : 0u) : 0u));
-    L.U = o;  o = al128(o + (uint32_t)(TPC * 32 * jcap * usz));
-    L.K = o;  o = al128(o + (uint32_t)(jcap * kD * isz));
-    L.Gs = o; o = al128(o + (uint32_t)(((jcap + 3) & ~3) * 4));
-    L.q = o;  o = al128(o + (uint32_t)(nt * kD * isz));
-    L.k = o;  o = al128(o + (uint32_t)(nt * kD * isz));
-    L.v = o;  o = al128(o + (uint32_t)(nt * TPC * 32 * isz));
-    L.kq32 = o; o = al128(o + (nt > 1 && isz == 2 ? (uint32_t)(nt * 2 * kD * 4) : 0u));   // fp32 k_t, q_t
-    L.Ck = o; o = al128(o + (uint32_t)(nt * J * 4));
-    L.Cq = o; o = al128(o + (uint32_t)(nt * J * 4));
-    L.av = o; o = al128(o + (uint32_t)(has_state ? TPC * nt * 32 * 4 : 0));
-    L.bv = o; o = al128(o + (uint32_t)(has_state ? TPC * nt * 32 * 4 : 0));
-    L.Gn = o; o = al128(o + (uint32_t)(nt * 4));
-    L.Bn = o; o = al128(o + (uint32_t)(nt * 4));
-    L.Y = o;  o = al128(o + (tc ? (uint32_t)(tc_nmma(nt) * kD * 4 * (isz == 4 ? 2 : 1)) : 0u));
-    L.Kf = o; o = al128(o + (fold ? (uint32_t)(J * kD * 4) : 0u));   // fused fold: fp32 keys
-    L.bar = o; o += 64;
-    L.bytes = al128(o);
-    return L;
-}
-
-// ---------------------------------------------------------------- row loads
-// A 4-lane team reduces one 128-wide row.  Lane `seg` (0..3) owns the eight
-// 16-byte column chunks ch(c) = seg + 4 (c ^ p), c < 8, where p is the row
-// parity of its team: the two rows read in one 128-bit shared-memory phase
-// (8 lanes) then touch 8 distinct bank groups.  k_t / q_t chunks are held in
-// registers in the same per-lane order, so the pairing is static.
-__device__ __forceinline__ int chunk_of(int seg, int p, int c) { return seg + 4 * (c ^ p); }
-
-template <typename T>
-__device__ __forceinline__ void load_row8(const T *row, int seg, int p, float4 (&x)[8]) {
-#pragma unroll
-    for (int c = 0; c < 8; ++c) x[c] = load4(row + 4 * chunk_of(seg, p, c));
-}
-
-__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
-    uint64_t d;
-    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d)
-        : "l"(*reinterpret_cast<uint64_t *>(&a)), "l"(*reinterpret_cast<uint64_t *>(&b)),
-          "l"(*reinterpret_cast<uint64_t *>(&c)));
-    return *reinterpret_cast<float2 *>(&d);
-}
-// sum_c x[c] . y[c] as two packed fp32 accumulators (SASS FFMA2)
-__device__ __forceinline__ float dot8x4(const float4 (&x)[8], const float4 (&y)[8]) {
-    float2 a0 = make_float2(0.f, 0.f), a1 = make_float2(0.f, 0.f);
-#pragma unroll
-    for (int c = 0; c < 8; ++c) {
-        a0 = ffma2(make_float2(x[c].x, x[c].y), make_float2(y[c].x, y[c].y), a0);
-        a1 = ffma2(make_float2(x[c].z, x[c].w), make_float2(y[c].z, y[c].w), a1);
-    }
-    return (a0.x + a0.y) + (a1.x + a1.y);
-}
-
-// Sum V values over the 4 lanes of a team (xor 1, 2).  V < 4: every lane gets
-// every sum, returned for value index x = seg (lanes seg >= V get -1).
-// V >= 4: transposed butterfly, lane seg ends with the V/4 sums of value
-// indices x = i + (V/4) seg.
-template <int V>
-struct TeamOut {
-    static constexpr int N = V >= 4 ? V / 4 : 1;
-};
-template <int V>
-__device__ __forceinline__ void team_reduce(float (&v)[V], int seg, float (&res)[TeamOut<V>::N],
-                                            int (&xid)[TeamOut<V>::N]) {
-    if constexpr (V < 4) {
-#pragma unroll
-        for (int j = 0; j < V; ++j) {
-            float x = v[j];
-            x += __shfl_xor_sync(0xffffffffu, x, 1);
-            x += __shfl_xor_sync(0xffffffffu, x, 2);
-            v[j] = x;
-        }
-        float r = v[0];
-#pragma unroll
-        for (int j = 1; j < V; ++j)
-            if (seg == j) r = v[j];
-        res[0] = r;
-        xid[0] = seg < V ? seg : -1;
-    } else {
-        int n = V;
-#pragma unroll
-        for (int s = 2; s >= 1; s >>= 1) {
-            const bool upper = (seg & s) != 0;
-            const int h = n / 2;
-#pragma unroll
-            for (int i = 0; i < V / 2; ++i) {
-                if (i < h) {
-                    const float send = upper ? v[i] : v[i + h];
-                    const float keep = upper ? v[i + h] : v[i];
-                    v[i] = keep + __shfl_xor_sync(0xffffffffu, send, s);
-                }
-            }
-            n = h;
-        }
-#pragma unroll
-        for (int i = 0; i < V / 4; ++i) {
-            res[i] = v[i];
-            xid[i] = i + (V / 4) * seg;
-        }
-    }
-}
-
-// TC (multi-token kinds with a state): the state mat-vecs a_t = S0 k_t,
-// b_t = S0 q_t of all new tokens are ONE M = 128 (d_v rows) x N (k_t, q_t
-// columns) x K = 128 contraction on the tensor cores: the state tile arrives
-// by 2-D TMA in the 128-byte-swizzled K-major layout the MMA reads, the
-// tokens are staged K-major, and fp32 accuracy comes from split TF32 (the
-// MMA reads the top 19 bits; pass 2 multiplies the exact remainder
-// S0 - trunc(S0), written in place once pass 1 has read the tile; fp32
-// tokens add a pass with their own remainder).
-__device__ __forceinline__ float trunc_tf32(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
-
-// FOLD (decode with auto-flush, la_set_auto_flush): when the step fills the
-// slot's buffer (J == C), the CTA -- which holds the S0 rows of its tiles,
-// every buffered key and its rows' delta values -- folds the C records into
-// those rows itself (P:407 on CUDA cores, fp32), and writes S_new: the
-// separate flush, and its second read of the state, disappear.
-constexpr int kFusedFoldMaxC = 32;
-// new tokens from which the state mat-vecs run on the tensor cores
-constexpr int kTcMinTokens = 8;
-
-template <typename InT, typename UT, int TPC, int WPT, int NT, bool HAS_STATE, int MINB, bool TC, bool FOLD = false>
-__global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const ChunkArgs a,
-                                                                        const __grid_constant__ CUtensorMap tmap) {
-    static_assert(!TC || (HAS_STATE && TPC == 4 && WPT == 1), "tensor-core pass: whole head per CTA");
-    static_assert(!FOLD || (NT == 1 && HAS_STATE && WPT == 1 && !TC), "fused fold: decode kind only");
-    constexpr int NMMA = tc_nmma(NT);
-    constexpr int NTHR = TPC * WPT * 32;
-    constexpr int RPW = 32 / WPT;                // d_v rows per warp
-    constexpr int V = 2 * NT;                    // reduced values per row: (k_t, q_t) dots
-    constexpr int NOUT = TeamOut<V>::N;
-    constexpr bool KQ_REG = NT == 1;             // k_t, q_t chunks held in registers
-    constexpr int isz = (int)sizeof(InT), usz = (int)sizeof(UT);
-    static_assert(NT <= 32, "decay scan runs inside one warp");
-    static_assert(NTHR >= 64, "warp 0 requests the records, warp 1 the new tokens");
-
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int seg = lane & 3, team = lane >> 2, par = team & 1;
-    const int wt = warp / WPT, half = warp % WPT;  // the warp's d_v tile and row block in it
-    const Dims dm = a.dm;
-    const int Hv = dm.Hv, Hk = dm.Hk;
-    const int tg = blockIdx.x, h = blockIdx.y, zi = blockIdx.z;
-    // index-array batches: the slot and the caller's input row of CTA row zi
-    // (staged by a previous grid: L2 loads, and never before the PDL wait --
-    // the host clears pdl_early for list launches)
-    const int r = a.slots ? __ldcg(a.slots + zi) : a.first + zi, hk = h / dm.g;
-    const int xrow = a.pos ? __ldcg(a.pos + zi) : zi;
-    const size_t sb = a.p.sidx ? (size_t)__ldcg(a.p.sidx + r) : (size_t)r;   // state slot
-    const int tile0 = tg * TPC;                  // first 32-row d_v tile of the CTA
-    const int n_new = a.n_new;
-    const bool direct = (a.kind == CK_DIRECT);
-    const int Jst = a.j0_cap + NT;               // row stride of Ck/Cq
-
-    extern __shared__ __align__(1024) unsigned char smem[];
-    const CtaLayout L = cta_layout(TPC, NT, HAS_STATE, a.j0_cap, isz, usz, TC, FOLD);
-    uint64_t *full = reinterpret_cast<uint64_t *>(smem + L.bar);
-    uint64_t *recs = full + 1;                  // second barrier: the buffered records
-    int *j0_s = reinterpret_cast<int *>(smem + L.bar + 16);
-    uint64_t *mmab = full + 3;                  // tensor-core pass completions
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + L.bar + 32);
-    unsigned char *S_base = smem + L.S;
-    if constexpr (TC) S_base += (1024u - (smem_u32(S_base) & 1023u)) & 1023u;
-    const float *S_s = reinterpret_cast<const float *>(S_base);
-    const UT *U_s = reinterpret_cast<const UT *>(smem + L.U);
-    const InT *K_s = reinterpret_cast<const InT *>(smem + L.K);
-    const float *G_s = reinterpret_cast<const float *>(smem + L.Gs);
-    const InT *q_s = reinterpret_cast<const InT *>(smem + L.q);
-    const InT *k_s = reinterpret_cast<const InT *>(smem + L.k);
-    const InT *v_s = reinterpret_cast<const InT *>(smem + L.v);
-    float *Ck = reinterpret_cast<float *>(smem + L.Ck);
-    float *Cq = reinterpret_cast<float *>(smem + L.Cq);
-    float *av = reinterpret_cast<float *>(smem + L.av);
-    float *bv = reinterpret_cast<float *>(smem + L.bv);
-    float *Gn_s = reinterpret_cast<float *>(smem + L.Gn);
-    float *Bn_s = reinterpret_cast<float *>(smem + L.Bn);
-
-    const InT *qin = static_cast<const InT *>(a.q);
-    const InT *kin = static_cast<const InT *>(a.k);
-    const InT *vin = static_cast<const InT *>(a.v);
-    auto tok_of = [&](int t) { return (size_t)xrow * a.tok_total + a.tok_offset + t; };
-
-    // ---- 0. Two mbarriers.  `full`: the fixed-size operands (state tiles,
-    //         new tokens), requested at once (thread 0: the state, warp 1:
-    //         q_t, k_t, v_t).  `recs`: the buffered records (U, K, G), which
-    //         need the slot's count j0; thread 0 alone reads it, requests the
-    //         records and publishes j0 through `recs`, then takes the slot
-    //         ticket (every CTA of the slot has read the counter before the
-    //         last ticket is drawn).  The state mat-vecs run while the records
-    //         are still in flight.
-    const uint32_t fixed_bytes = (HAS_STATE ? (uint32_t)(TPC * 32 * kD * 4) : 0u) +
-                                 (uint32_t)(n_new * (2 * kD * isz + TPC * 32 * isz));
-    auto issue_state = [&]() {
-        if constexpr (TC) {   // four 128-row x 32-column boxes, 128-byte swizzle
-            const int row0 = (int)((sb * Hv + h) * kD);
-#pragma unroll
-            for (int kb = 0; kb < 4; ++kb) tma_load_2d(S_base + kb * (TPC * 32 * 128), &tmap, kb * 32, row0, full);
-        } else {
-            bulk_g2s(smem + L.S, a.p.state + ((sb * Hv + h) * kD + (size_t)tile0 * 32) * kD,
-                     TPC * 32 * kD * 4, full);
-        }
-    };
-    if constexpr (TC) {
-        if (warp == 0) tmem_alloc<32>(tmem_slot);
-    }
-    if (tid == 0) {
-        mbar_init(full, 1);
-        mbar_init(recs, 1);
-        if (TC) mbar_init(mmab, 1);
-        fence_mbar_init();
-        if (HAS_STATE && a.pdl_early) {
-            // the state tile is not written by the grid this one overlaps
-            // (launch overlap), so it streams in while that grid drains
-            mbar_arrive_expect_tx(full, fixed_bytes);
-            issue_state();
-        }
-    }
-    if (a.pdl) pdl_wait();   // inputs, counters and records may come from the previous grid
-    pdl_trigger();
-    // alpha / beta of the new tokens (lane t), in flight with the copies
-    float al_l = 1.f, be_l = 0.f;
-    if (lane < n_new) {
-        al_l = a.alpha[tok_of(lane) * Hv + h];
-        be_l = a.beta[tok_of(lane) * Hv + h];
-    }
-    __syncthreads();
-    int ticket = 0;
-    if (warp == 0) {
-        // lane 0: the state (unless early), the slot's count j0; the j0-dependent
-        // records are requested by the lanes in parallel, one copy per (record
-        // block, field): the tiles' u sub-tiles, the QK head's key rows, the
-        // log decays (contiguous handles: a single block)
-        int j0v = 0;
-        if (lane == 0) {
-            if (!(HAS_STATE && a.pdl_early)) {
-                mbar_arrive_expect_tx(full, fixed_bytes);
-                if (HAS_STATE) issue_state();
-            }
-            j0v = (direct ? a.p.len : a.p.occ)[r] + a.j_add;
-            *j0_s = j0v;
-        }
-        j0v = __shfl_sync(0xffffffffu, j0v, 0);
-        const int bt = dm.bt, nb = (j0v + bt - 1) / bt;
-        if (lane == 0) {
-            uint32_t gbytes = 0;
-            for (int b = 0; b < nb; ++b) gbytes += (uint32_t)(((min(bt, j0v - b * bt) + 3) & ~3) * 4);
-            mbar_arrive_expect_tx(recs, (uint32_t)(TPC * 32 * j0v * usz) + (uint32_t)(j0v * kD * isz) + gbytes);
-        }
-        __syncwarp();
-        constexpr int NF = TPC + 2;
-        for (int c = lane; c < nb * NF; c += 32) {
-            const int b = c / NF, f = c % NF, cnt = min(bt, j0v - b * bt);
-            const size_t blk = a.p.btab ? (size_t)__ldcg(a.p.btab + (size_t)r * dm.maxb + b) : (size_t)r;
-            if (f < TPC)
-                bulk_g2s(smem + L.U + ((size_t)f * j0v + (size_t)b * bt) * kUSub * usz,
-                         static_cast<const UT *>(a.p.U) + (((blk * Hv + h) * (kD / kUSub) + tile0 + f) * bt) * kUSub,
-                         (uint32_t)(cnt * kUSub * usz), recs);
-            else if (f == TPC)
-                bulk_g2s(smem + L.K + (size_t)b * bt * kD * isz,
-                         static_cast<const InT *>(a.p.K) + (blk * Hk + hk) * bt * kD, (uint32_t)(cnt * kD * isz), recs);
-            else
-                bulk_g2s(smem + L.Gs + (size_t)b * bt * 4, a.p.G + (blk * Hv + h) * bt,
-                         (uint32_t)(((cnt + 3) & ~3) * 4), recs);
-        }
-        if (lane == 0 && a.kind != CK_VERIFY) ticket = atomicAdd(&a.p.ticket[r], 1);
-    } else if (warp == 1) {
-        // new tokens: q_t, k_t rows of the QK head and the tiles' v_t slice
-        // (warp 1's lanes, so they issue in parallel with warp 0)
-        for (int c = lane; c < 3 * n_new; c += 32) {
-            const int t = c % n_new, kind = c / n_new;
-            if (kind == 0)
-                bulk_g2s(smem + L.q + (size_t)t * kD * isz, qin + (tok_of(t) * Hk + hk) * kD, kD * isz, full);
-            else if (kind == 1)
-                bulk_g2s(smem + L.k + (size_t)t * kD * isz, kin + (tok_of(t) * Hk + hk) * kD, kD * isz, full);
-            else
-                bulk_g2s(smem + L.v + (size_t)t * TPC * 32 * isz, vin + (tok_of(t) * Hv + h) * kD + tile0 * 32,
-                         TPC * 32 * isz, full);
-        }
-    }
-
-    // ---- 1. cumulative log decay increments of the new tokens (lane t), in registers
-    unsigned bad = 0;
-    float x_l = 0.f;
-    if (lane < n_new) {
-        x_l = logf(al_l);
-        if (dm.validate && warp == 0) {
-            if (!(al_l > 0.f && al_l <= 1.f)) bad |= 0x1u;
-            if (!(be_l >= 0.f && be_l <= 1.f)) bad |= 0x2u;
-        }
-    }
-#pragma unroll
-    for (int off = 1; off < NT; off <<= 1) {
-        const float y = __shfl_up_sync(0xffffffffu, x_l, off);
-        if (lane >= off) x_l += y;
-    }
-    mbar_wait(full, 0);
-    // multi-token launches read k_t / q_t once per row step: widen them to
-    // fp32 once per CTA ([t][k | q][128])
-    constexpr bool KQ32 = !KQ_REG && isz == 2;
-    float *kq32 = reinterpret_cast<float *>(smem + L.kq32);
-    if constexpr (KQ32) {
-        for (int e = tid; e < n_new * kD; e += NTHR) {
-            const int t = e / kD, c = e % kD;
-            kq32[(t * 2 + 0) * kD + c] = to_f(k_s[e]);
-            kq32[(t * 2 + 1) * kD + c] = to_f(q_s[e]);
-        }
-        __syncthreads();
-    }
-    uint32_t tmem = 0;
-    float *Yh = reinterpret_cast<float *>(smem + L.Y);
-    float *Yl = Yh + NMMA * kD;
-    auto mma_pass = [&](const float *Y, bool acc) {
-        const uint32_t idesc = idesc_tf32(128, NMMA);
-#pragma unroll
-        for (int kk = 0; kk < kD / 8; ++kk) {
-            const uint64_t da = umma_desc_sw128(smem_u32(S_base) + (kk >> 2) * (TPC * 32 * 128) + (kk & 3) * 32);
-            const uint64_t db = umma_desc_noswz(smem_u32(Y) + kk * 256, 128, kD * 32);
-            tc_mma_tf32(tmem, da, db, idesc, (acc || kk > 0) ? 1u : 0u);
-        }
-    };
-    if constexpr (TC) {
-        // B operand: row n = (k_t | q_t) of token n / 2, K-major SWIZZLE_NONE
-        // (8-row x 16-byte core matrices, K-adjacent at +128 B, row groups at +4 KiB)
-        for (int e = tid; e < NMMA * kD; e += NTHR) {
-            const int n = e / kD, c = e % kD, t = n >> 1;
-            float x = 0.f;
-            if (t < n_new) x = to_f(((n & 1) ? q_s : k_s)[t * kD + c]);
-            const int off = (n >> 3) * (kD * 32 / 4) + (c >> 2) * 32 + (n & 7) * 4 + (c & 3);
-            if constexpr (isz == 4) {
-                const float hi = trunc_tf32(x);
-                Yh[off] = hi;
-                Yl[off] = x - hi;
-            } else {
-                Yh[off] = x;     // bf16 values are exact in tf32
-            }
-        }
-        fence_proxy_async_smem();
-        tc_fence_before();
-        __syncthreads();
-        tc_fence_after();
-        tmem = *tmem_slot;
-        if (tid == 0) {
-            mma_pass(Yh, false);                    // trunc(S0) . Y_hi
-            if constexpr (isz == 4) mma_pass(Yl, true);   // trunc(S0) . Y_lo
-            tc_commit(mmab);
-        }
-    }
-    int j0 = 0, J = 0;
-    float gn_l = 0.f;
-    // ---- 2. rows with 4-lane teams, 8 rows per warp step:
-    //      state rows of the warp's tile: a = S0 k_t, b = S0 q_t;
-    //      key rows i (shared out over the warps):
-    //        Ck[t][i] = e^{G_t-G_i} (k_t.k_i) (i < j0+t),  Cq[t][i] = e^{G_t-G_i} (q_t.k_i) (i <= j0+t)  (Z3)
-    {
-        float4 kx[KQ_REG ? 8 : 1], qx[KQ_REG ? 8 : 1];
-        if constexpr (KQ_REG) {
-            load_row8(k_s, seg, par, kx);
-            load_row8(q_s, seg, par, qx);
-        }
-        // dots of row x with k_t and q_t (this lane's 32 columns)
-        auto row_dots = [&](const float4 (&x)[8], float (&vals)[V]) {
-            if constexpr (KQ_REG) {
-                vals[0] = dot8x4(x, kx);
-                vals[1] = dot8x4(x, qx);
-            } else {
-#pragma unroll
-                for (int t = 0; t < NT; ++t) {
-                    float4 y[8];
-                    if constexpr (KQ32) load_row8(kq32 + (size_t)(t * 2) * kD, seg, par, y);
-                    else load_row8(k_s + (size_t)t * kD, seg, par, y);
-                    vals[2 * t] = dot8x4(x, y);
-                    if constexpr (KQ32) load_row8(kq32 + (size_t)(t * 2 + 1) * kD, seg, par, y);
-                    else load_row8(q_s + (size_t)t * kD, seg, par, y);
-                    vals[2 * t + 1] = dot8x4(x, y);
-                }
-            }
-        };
-        // state rows of the warp's tile: 4 steps of 8 rows (one token), or --
-        // when k_t / q_t come from shared memory (several tokens) -- 2 steps
-        // of 2 x 8 rows, so every k_t / q_t chunk load serves two rows
-        if constexpr (TC) {
-            // (the tensor-core pass is in flight; see after the key rows)
-        } else if constexpr (HAS_STATE && KQ_REG) {
-#pragma unroll 4
-            for (int st = 0; st < RPW / 8; ++st) {
-                const int rf = half * RPW + st * 8 + team;
-                float4 x[8];
-                load_row8(S_s + (size_t)(wt * 32 + rf) * kD, seg, par, x);
-                float vals[V];
-                row_dots(x, vals);
-                float res[NOUT];
-                int xid[NOUT];
-                team_reduce<V>(vals, seg, res, xid);
-#pragma unroll
-                for (int o = 0; o < NOUT; ++o) {
-                    const int t = xid[o] >> 1;
-                    if (xid[o] >= 0 && t < n_new) ((xid[o] & 1) ? bv : av)[(wt * NT + t) * 32 + rf] = res[o];
-                }
-            }
-        } else if constexpr (HAS_STATE && V <= 8 && WPT == 1) {
-            // 2 or 4 new tokens (verify): lane owns columns 4 lane .. 4 lane + 3 of
-            // all V = 2 NT vectors (k_t, q_t) in registers and reads whole state
-            // rows (one conflict-free 16-byte read per row); RB = 32 / V rows per
-            // batch give 32 partial sums per lane, summed across the warp by one
-            // transposed butterfly (lane l ends with value l = (row l / V, vector l % V))
-            constexpr int RB = 32 / V;
-            float4 vec[V];
-#pragma unroll
-            for (int v = 0; v < V; ++v) {
-                if constexpr (KQ32) vec[v] = *reinterpret_cast<const float4 *>(kq32 + (size_t)v * kD + 4 * lane);
-                else vec[v] = load4(((v & 1) ? q_s : k_s) + (size_t)(v >> 1) * kD + 4 * lane);
-            }
-#pragma unroll 1
-            for (int rb = 0; rb < 32; rb += RB) {
-                float vals[32];
-#pragma unroll
-                for (int rr = 0; rr < RB; ++rr) {
-                    const float4 s4 = *reinterpret_cast<const float4 *>(S_s + (size_t)(wt * 32 + rb + rr) * kD + 4 * lane);
-#pragma unroll
-                    for (int v = 0; v < V; ++v)
-                        vals[rr * V + v] = fmaf(s4.x, vec[v].x, fmaf(s4.y, vec[v].y, fmaf(s4.z, vec[v].z, s4.w * vec[v].w)));
-                }
-                const float red = transposed_reduce<32>(vals, lane);
-                const int row = rb + lane / V, v = lane % V, t = v >> 1;
-                if (t < n_new) ((v & 1) ? bv : av)[(wt * NT + t) * 32 + row] = red;
-            }
-        } else if constexpr (HAS_STATE) {
-            static_assert(RPW % 16 == 0, "two row blocks per step");
-            constexpr int NOUT2 = TeamOut<2 * V>::N;
-            for (int st = 0; st < RPW / 16; ++st) {
-                const int rf0 = half * RPW + st * 16 + team, rf1 = rf0 + 8;
-                float4 x0[8], x1[8];
-                load_row8(S_s + (size_t)(wt * 32 + rf0) * kD, seg, par, x0);
-                load_row8(S_s + (size_t)(wt * 32 + rf1) * kD, seg, par, x1);
-                float vals[2 * V];
-#pragma unroll
-                for (int t = 0; t < NT; ++t) {
-                    float4 y[8];
-                    if constexpr (KQ32) load_row8(kq32 + (size_t)(t * 2) * kD, seg, par, y);
-                    else load_row8(k_s + (size_t)t * kD, seg, par, y);
-                    vals[2 * t] = dot8x4(x0, y);
-                    vals[V + 2 * t] = dot8x4(x1, y);
-                    if constexpr (KQ32) load_row8(kq32 + (size_t)(t * 2 + 1) * kD, seg, par, y);
-                    else load_row8(q_s + (size_t)t * kD, seg, par, y);
-                    vals[2 * t + 1] = dot8x4(x0, y);
-                    vals[V + 2 * t + 1] = dot8x4(x1, y);
-                }
-                float res[NOUT2];
-                int xid[NOUT2];
-                team_reduce<2 * V>(vals, seg, res, xid);
-#pragma unroll
-                for (int o = 0; o < NOUT2; ++o) {
-                    const int xv = xid[o] % V, rf = xid[o] < V ? rf0 : rf1;
-                    const int t = xv >> 1;
-                    if (xid[o] >= 0 && t < n_new) ((xv & 1) ? bv : av)[(wt * NT + t) * 32 + rf] = res[o];
-                }
-            }
-        }
-        // ---- the buffered records: j0, log decays
-        mbar_wait(recs, 0);
-        j0 = *j0_s;
-        J = j0 + n_new;
-        gn_l = (j0 > 0 ? G_s[j0 - 1] : 0.f) + x_l;
-        if (warp == 0 && lane < n_new) {
-            Gn_s[lane] = gn_l;
-            Bn_s[lane] = be_l;
-        }
-        // key rows, shared out over the warps in steps of 8
-        const int KS = (J + 7) / 8;
-        for (int ks = warp; ks < KS; ks += TPC * WPT) {
-            const int i = ks * 8 + team;
-            float4 x[8];
-            if (i < J) {
-                load_row8(i < j0 ? K_s + (size_t)i * kD : k_s + (size_t)(i - j0) * kD, seg, par, x);
-            } else {
-#pragma unroll
-                for (int c = 0; c < 8; ++c) x[c] = make_float4(0.f, 0.f, 0.f, 0.f);
-            }
-            float vals[V];
-            row_dots(x, vals);
-            float res[NOUT];
-            int xid[NOUT];
-            team_reduce<V>(vals, seg, res, xid);
-            const int inew = (i - j0) > 0 ? (i - j0) : 0;
-#pragma unroll
-            for (int o = 0; o < NOUT; ++o) {
-                const int t = xid[o] >= 0 ? (xid[o] >> 1) : 0;
-                const bool isq = xid[o] & 1;
-                const float gt = __shfl_sync(0xffffffffu, gn_l, t);
-                const float gnew = __shfl_sync(0xffffffffu, gn_l, inew < NT ? inew : 0);
-                if (xid[o] >= 0 && i < J && t < n_new) {
-                    const bool valid = isq ? (i <= j0 + t) : (i < j0 + t);
-                    float cf = 0.f;
-                    if (valid) cf = expf(gt - (i < j0 ? G_s[i] : gnew)) * res[o];
-                    (isq ? Cq : Ck)[t * Jst + i] = cf;
-                }
-            }
-        }
-    }
-    if constexpr (TC) {
-        // pass 2 on the exact remainder S0 - trunc(S0), written in place once
-        // pass 1 has read the tile (the split is elementwise: layout-agnostic)
-        mbar_wait(mmab, 0);
-        float4 *S4 = reinterpret_cast<float4 *>(S_base);
-        for (int e = tid; e < TPC * 32 * kD / 4; e += NTHR) {
-            float4 x = S4[e];
-            x.x -= trunc_tf32(x.x);
-            x.y -= trunc_tf32(x.y);
-            x.z -= trunc_tf32(x.z);
-            x.w -= trunc_tf32(x.w);
-            S4[e] = x;
-        }
-        fence_proxy_async_smem();
-        __syncthreads();
-        if (tid == 0) {
-            tc_fence_after();
-            mma_pass(Yh, true);                     // (S0 - trunc(S0)) . Y_hi
-            tc_commit(mmab);
-        }
-        mbar_wait(mmab, 1);
-        tc_fence_after();
-        // D row m = d_v row 32 w + lane: warp w reads TMEM lanes 32w..32w+31
-        float dv[32];
-        tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16), dv);
-#pragma unroll
-        for (int t = 0; t < NT; ++t) {
-            if (t < n_new) {
-                av[(warp * NT + t) * 32 + lane] = dv[2 * t];
-                bv[(warp * NT + t) * 32 + lane] = dv[2 * t + 1];
-            }
-        }
-    }
-    if (dm.validate) {
-        for (int e = tid; e < n_new * kD; e += NTHR) {
-            const float kk = to_f(k_s[e]), qq = to_f(q_s[e]);
-            if (!(isfinite(kk) && isfinite(qq))) bad |= 0x4u;
-        }
-    }
-    if constexpr (TC) tc_fence_before();
-    __syncthreads();
-    if constexpr (TC) {
-        if (warp == 0) {
-            tc_fence_after();
-            tmem_dealloc<32>(tmem);
-        }
-    }
-
-    // ---- 3. forward substitution over the new tokens.  Lane -> d_v row
-    //         (half * RPW + lane % RPW) of the warp's tile; the WPT lanes of a
-    //         row split the buffered records by i % WPT and combine by shuffle.
-    {
-        const int sub = lane / RPW, row = half * RPW + lane % RPW, tile = tile0 + wt;
-        const int drow = tile * 32 + row;
-        const UT *ut = U_s + (size_t)wt * j0 * kUSub + row;
-        // record position j0 + t of the slot: (block, offset)
-        auto recpos = [&](int t) -> int2 {
-            if (!a.p.btab) return make_int2(r, j0 + t);
-            return make_int2(__ldcg(a.p.btab + (size_t)r * dm.maxb + (j0 + t) / dm.bt), (j0 + t) % dm.bt);
-        };
-        float un[NT];
-#pragma unroll
-        for (int t = 0; t < NT; ++t) {
-            if (t < n_new) {
-                const float *ck = Ck + t * Jst;
-                const float *cq = Cq + t * Jst;
-                float ak0 = 0.f, ak1 = 0.f, aq0 = 0.f, aq1 = 0.f;
-                int i = sub;
-                for (; i + WPT < j0; i += 2 * WPT) {
-                    const float u0 = to_f(ut[(size_t)i * kUSub]);
-                    const float u1 = to_f(ut[(size_t)(i + WPT) * kUSub]);
-                    ak0 = fmaf(ck[i], u0, ak0);
-                    aq0 = fmaf(cq[i], u0, aq0);
-                    ak1 = fmaf(ck[i + WPT], u1, ak1);
-                    aq1 = fmaf(cq[i + WPT], u1, aq1);
-                }
-                if (i < j0) {
-                    const float u0 = to_f(ut[(size_t)i * kUSub]);
-                    ak0 = fmaf(ck[i], u0, ak0);
-                    aq0 = fmaf(cq[i], u0, aq0);
-                }
-                float acc_k = ak0 + ak1, acc_q = aq0 + aq1;
-#pragma unroll
-                for (int m = RPW; m < 32; m <<= 1) {
-                    acc_k += __shfl_xor_sync(0xffffffffu, acc_k, m);
-                    acc_q += __shfl_xor_sync(0xffffffffu, acc_q, m);
-                }
-#pragma unroll
-                for (int tp = 0; tp < t; ++tp) {
-                    acc_k = fmaf(ck[j0 + tp], un[tp], acc_k);
-                    acc_q = fmaf(cq[j0 + tp], un[tp], acc_q);
-                }
-                const float vt = to_f(v_s[t * TPC * 32 + wt * 32 + row]);
-                const float bt = Bn_s[t];
-                const float eG = expf(Gn_s[t]);
-                float u, o;
-                if (HAS_STATE) {
-                    u = bt * (vt - fmaf(eG, av[(wt * NT + t) * 32 + row], acc_k));
-                    o = fmaf(eG, bv[(wt * NT + t) * 32 + row], acc_q);
-                } else {
-                    u = bt * (vt - acc_k);
-                    o = acc_q;
-                }
-                const UT us = from_f<UT>(u);
-                un[t] = to_f(us);                      // the stored (rounded) value
-                o = fmaf(cq[j0 + t], un[t], o);
-                if (sub == 0) {
-                    if (dm.validate && !isfinite(vt)) bad |= 0x4u;
-                    if (a.o) a.o[(tok_of(t) * Hv + h) * kD + drow] = o;
-                    const int2 rp = recpos(t);
-                    const size_t bh = (size_t)rp.x * Hv + h;
-                    static_cast<UT *>(a.p.U)[((bh * (kD / kUSub) + tile) * dm.bt + rp.y) * kUSub + row] = us;
-                    if (dm.keep_raw) {
-                        static_cast<InT *>(a.p.V)[(bh * dm.bt + rp.y) * kD + drow] = v_s[t * TPC * 32 + wt * 32 + row];
-                        if (tile == 0 && row == 0) a.p.B[bh * dm.bt + rp.y] = bt;
-                    }
-                }
-            }
-        }
-        if constexpr (FOLD) {
-            if (J == dm.C) {   // CTA-uniform
-                // the J keys as fp32 rows, once per CTA
-                float *Kf = reinterpret_cast<float *>(smem + L.Kf);
-                for (int e = tid; e < J * kD; e += NTHR)
-                    Kf[e] = to_f(e < j0 * kD ? K_s[e] : k_s[e - j0 * kD]);
-                // this thread's state row: S_new = e^{G_t} S0 + sum_{i<J} e^{G_t-G_i} u_i k_i^T
-                const float gt = Gn_s[0];
-                float coef[kFusedFoldMaxC];
-#pragma unroll
-                for (int i = 0; i < kFusedFoldMaxC; ++i)
-                    coef[i] = i < j0 ? expf(gt - G_s[i]) * to_f(ut[(size_t)i * kUSub]) : (i == j0 ? un[0] : 0.f);
-                const float eG = expf(gt);
-                float *Srow = const_cast<float *>(S_s) + (size_t)(wt * 32 + row) * kD;
-                __syncthreads();
-                // rotated 16-byte chunks: the lanes (rows) hit distinct bank groups of
-                // the state rows and sweep each key row once; packed FFMA2
-                for (int cc = 0; cc < kD / 4; ++cc) {
-                    const int c4 = 4 * ((cc + lane) & (kD / 4 - 1));
-                    const float4 s4 = *reinterpret_cast<const float4 *>(Srow + c4);
-                    float2 s01 = make_float2(eG * s4.x, eG * s4.y), s23 = make_float2(eG * s4.z, eG * s4.w);
-#pragma unroll
-                    for (int i = 0; i < kFusedFoldMaxC; ++i) {
-                        if (i < J) {
-                            const float4 k4 = *reinterpret_cast<const float4 *>(Kf + i * kD + c4);
-                            const float2 cf = make_float2(coef[i], coef[i]);
-                            s01 = ffma2(cf, make_float2(k4.x, k4.y), s01);
-                            s23 = ffma2(cf, make_float2(k4.z, k4.w), s23);
-                        }
-                    }
-                    *reinterpret_cast<float4 *>(Srow + c4) = make_float4(s01.x, s01.y, s23.x, s23.y);
-                }
-            }
-        }
-    }
-    if constexpr (FOLD) {
-        if (J == dm.C) {   // CTA-uniform: one bulk store of the CTA's folded rows
-            fence_proxy_async_smem();
-            __syncthreads();
-            if (tid == 0) {
-                bulk_s2g(a.p.state + ((sb * Hv + h) * kD + (size_t)tile0 * 32) * kD, S_s, TPC * 32 * kD * 4);
-                bulk_commit();
-            }
-        }
-    }
-    // ---- 4. records: k_t once per QK head, G_t per V head (first tile group)
-    if (tg == 0) {
-        auto recpos = [&](int t) -> int2 {
-            if (!a.p.btab) return make_int2(r, j0 + t);
-            return make_int2(__ldcg(a.p.btab + (size_t)r * dm.maxb + (j0 + t) / dm.bt), (j0 + t) % dm.bt);
-        };
-        if (h % dm.g == 0) {
-            for (int idx = tid; idx < n_new * kD; idx += NTHR) {
-                const int2 rp = recpos(idx / kD);
-                static_cast<InT *>(a.p.K)[(((size_t)rp.x * Hk + hk) * dm.bt + rp.y) * kD + idx % kD] = k_s[idx];
-            }
-        }
-        if (tid < n_new) {
-            const int2 rp = recpos(tid);
-            a.p.G[((size_t)rp.x * Hv + h) * dm.bt + rp.y] = Gn_s[tid];
-        }
-    }
-    if (a.kind != CK_VERIFY && tid == 0 && ticket == (int)(gridDim.x * gridDim.y) - 1) {
-        a.p.ticket[r] = 0;
-        if (direct) a.p.len[r] = J;
-        else a.p.occ[r] = (FOLD && J == dm.C) ? 0 : J;
-    }
-    if (bad) atomicOr(a.p.status, bad);
-    if constexpr (FOLD) {
-        if (J == dm.C && tid == 0) bulk_wait_read0();   // shared memory stays live until the store has read it
-    }
-}
-
-// ---------------------------------------------------------------- launch
-template <typename InT, typename UT, int TPC, int WPT, int NT, bool HAS_STATE, int MBO = 0, bool TC = false,
-          bool FOLD = false>
-static cudaError_t launch_cfg(const ChunkArgs &a, cudaStream_t s) {
-    const CtaLayout L = cta_layout(TPC, NT, HAS_STATE, a.j0_cap, sizeof(InT), sizeof(UT), TC, FOLD);
-    if (L.bytes > 227 * 1024) return cudaErrorInvalidConfiguration;
-    if (a.n > kMaxSlotsPerLaunch) return cudaErrorInvalidConfiguration;
-    constexpr int MINB = MBO ? MBO : (NT <= 2 ? (HAS_STATE ? 12 / (TPC * WPT) : 2) : 1);
-    auto kfn = chunk_cta_kernel<InT, UT, TPC, WPT, NT, HAS_STATE, MINB < 1 ? 1 : MINB, TC, FOLD>;
-    cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.bytes);
-    if (e != cudaSuccess) return e;
-    if (a.dry) return cudaSuccess;   // configuration check only (all-or-nothing pre-pass)
-    CUtensorMap tm;
-    if (TC) tm = *static_cast<const CUtensorMap *>(a.tmap);
-    else memset(&tm, 0, sizeof(tm));
-    return launch_k(kfn, dim3(4 / TPC, a.dm.Hv, a.n), dim3(TPC * WPT * 32), L.bytes, s, a.pdl != 0, a, tm);
-}
-
-template <typename InT, typename UT, int TPC, int WPT, bool HAS_STATE, int MBO = 0, bool TC = false>
-static cudaError_t launch_nt(const ChunkArgs &a, cudaStream_t s) {
-    if (!TC && a.n_new == 1) return launch_cfg<InT, UT, TPC, WPT, 1, HAS_STATE, MBO, TC>(a, s);
-    if (a.n_new <= 2) return launch_cfg<InT, UT, TPC, WPT, 2, HAS_STATE, MBO, TC>(a, s);
-    if (a.n_new <= 4) return launch_cfg<InT, UT, TPC, WPT, 4, HAS_STATE, MBO, TC>(a, s);
-    if (a.n_new <= 8) return launch_cfg<InT, UT, TPC, WPT, 8, HAS_STATE, MBO, TC>(a, s);
-    return launch_cfg<InT, UT, TPC, WPT, 16, HAS_STATE, MBO, TC>(a, s);
-}
-
-template <typename InT, typename UT>
-static cudaError_t launch_t(const ChunkArgs &a, cudaStream_t s) {
-    // (1 or 4 tiles per CTA and 2 warps per tile were measured and rejected,
-    //  DESIGN.md section 6)
-    // direct: at most 128 registers so 4 CTAs (16 warps) share an SM (measured
-    // 338 -> 281 us at config 4; 5 CTAs spill more and lose); 2 warps per tile
-    // for the multi-token kinds was measured slower (195 -> 262-280 us)
-    if (a.kind == CK_DIRECT) return launch_nt<InT, UT, kDirectTPC, 1, false, 4>(a, s);
-    if (a.fold) {   // decode with the fused fold (host: some slot fills, C <= 32)
-        if (a.kind != CK_DECODE || a.n_new != 1 || a.dm.C > kFusedFoldMaxC) return cudaErrorInvalidValue;
-        return launch_cfg<InT, UT, kChunkTPC, 1, 1, true, 0, false, true>(a, s);
-    }
-    // 8 or more new tokens (verify with N >= 8, prefill chunks): the state
-    // mat-vecs on the tensor cores, one CTA per (slot, V head).  Measured at
-    // batch 256 (tools/time_verify.py): N = 2 / 4 / 8 -> 197 / 224 / 290 us
-    // vs 107 / 189 / 322 us on the CUDA cores.
-    if (a.n_new >= kTcMinTokens && a.tmap) return launch_nt<InT, UT, 4, 1, true, 1, true>(a, s);
-    return launch_nt<InT, UT, kChunkTPC, 1, true>(a, s);
-}
-
-cudaError_t launch_chunk(const ChunkArgs &a_in, cudaStream_t s, int64_t *launches) {
-    if (a_in.n <= 0 || a_in.n_new <= 0) return cudaSuccess;
-    const ChunkArgs &a = a_in;
+cudaError_t launch_chunk(const ChunkArgs &a, cudaStream_t s, int64_t *launches) {
+    if (a.n <= 0 || a.n_new <= 0) return cudaSuccess;
     if (a.n_new > max_new_per_launch(a.dm.g)) return cudaErrorInvalidValue;
+    const bool direct = a.kind == CK_DIRECT;
     cudaError_t e;
     if (a.dm.in_dt == DT_F32)
-        e = launch_t<float, float>(a, s);
+        e = direct ? launch_direct_f32(a, s) : launch_state_f32(a, s);
     else if (a.dm.u_dt == DT_F16)
-        e = launch_t<__nv_bfloat16, __half>(a, s);
+        e = direct ? launch_direct_bf16h(a, s) : launch_state_bf16h(a, s);
     else
-        e = launch_t<__nv_bfloat16, float>(a, s);
+        e = direct ? launch_direct_bf16(a, s) : launch_state_bf16(a, s);
     if (e == cudaSuccess && !a.dry) ++*launches;
     return e;
 }

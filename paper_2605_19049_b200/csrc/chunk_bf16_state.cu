@@ -1,0 +1,7 @@
+// chunk_bf16_state.cu — one (dtype, kind) slice of the chunk-attend kernel instantiations
+// (kernels (1), (3), (4) and the prefill chunk step; see chunk.cuh).
+#include "chunk.cuh"
+
+namespace labuf {
+cudaError_t launch_state_bf16(const ChunkArgs &a, cudaStream_t s) { return launch_state<__nv_bfloat16, float>(a, s); }
+}  // namespace labuf

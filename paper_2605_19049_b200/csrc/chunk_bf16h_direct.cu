@@ -1,0 +1,7 @@
+// chunk_bf16h_direct.cu — one (dtype, kind) slice of the chunk-attend kernel instantiations
+// (kernels (1), (3), (4) and the prefill chunk step; see chunk.cuh).
+#include "chunk.cuh"
+
+namespace labuf {
+cudaError_t launch_direct_bf16h(const ChunkArgs &a, cudaStream_t s) { return launch_direct<__nv_bfloat16, __half>(a, s); }
+}  // namespace labuf

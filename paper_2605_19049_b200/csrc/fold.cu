@@ -68,11 +68,14 @@ __device__ __forceinline__ uint32_t kmaj_off(int row, int k, int kc) {
 //                     - sum_{l<i} e^{G_i-G_l} (k_i.k_l) u_l[j])  (forward substitution)
 // i.e. U = T Diag(beta) (V - Diag(e^G) W) with T = [I + strictLower(Diag(beta)
 // (Gamma (.) K K^T))]^{-1}, then the same tensor-core fold as mode i.
-template <typename InT, typename UT, bool FP32_IN, int kFoldNJ, int KCM, bool RAW>
+template <typename InT, typename UT, bool FP32_IN, int kFoldNJ, int KCM, bool RAW, bool PG>
 __global__ void __launch_bounds__(kFoldThreads, RAW ? 4 : (kFoldNJ == 128 ? 2 : (kFoldNJ == 32 && KCM == 16 ? 8 : 4))) fold_kernel(const FoldArgs a) {
     constexpr int NPAR = kFoldThreads / kFoldNJ;   // token parities per B row
     const int jh = blockIdx.x, h = blockIdx.y, zi = blockIdx.z;
-    const int r = a.slots ? __ldcg(a.slots + zi) : a.first + zi;
+    if constexpr (PG) {   // slot lists, state indices and block tables may come from the previous grid
+        if (a.pdl) pdl_wait();
+    }
+    const int r = PG && a.slots ? __ldcg(a.slots + zi) : a.first + zi;
     const int tid = threadIdx.x, warp = tid >> 5;
     const Dims dm = a.dm;
     const int Hv = dm.Hv, bt = dm.bt;
@@ -87,8 +90,14 @@ __global__ void __launch_bounds__(kFoldThreads, RAW ? 4 : (kFoldNJ == 128 ? 2 : 
     uint64_t *bar_mma = bar_ld + 1;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bar_ld + 2);
     int *meta = reinterpret_cast<int *>(bar_ld + 3);      // n, zero_s0
-    const size_t sb = a.p.sidx ? (size_t)__ldcg(a.p.sidx + r) : (size_t)r;
+    const size_t sb = PG && a.p.sidx ? (size_t)__ldcg(a.p.sidx + r) : (size_t)r;
     float *state_tile = a.p.state + ((sb * Hv + h) * kD + (size_t)jh * kFoldNJ) * kD;
+    // where S_new goes: the slot's own state, or (FK_FORK) the destination slot's
+    float *state_out = state_tile;
+    if (a.kind == FK_FORK) {
+        const size_t db = PG && a.p.sidx ? (size_t)__ldcg(a.p.sidx + a.fork_dst) : (size_t)a.fork_dst;
+        state_out = a.p.state + ((db * Hv + h) * kD + (size_t)jh * kFoldNJ) * kD;
+    }
 
     // per-thread operand coordinates: A column c = tid (all KC tokens);
     // B row j = tid % NJ, tokens i = ip (mod NPAR)
@@ -97,16 +106,18 @@ __global__ void __launch_bounds__(kFoldThreads, RAW ? 4 : (kFoldNJ == 128 ? 2 : 
     // record i of the slot (block table or the slot's own region): key row,
     // this thread's delta value u_i[jr] (U is tile-major
     // [blk][Hv][d/kUSub][bt][kUSub]), log decay, raw value, beta
+    // (PG: block table lookups; else the slot's own region, block = slot)
+    auto at = [&](int i) -> int2 { return PG ? rec_at(dm, a.p, r, i) : make_int2(r, i); };
     auto rec = [&](int i) -> size_t {   // (block * Hv + h) * bt + offset
-        const int2 ba = rec_at(dm, a.p, r, i);
+        const int2 ba = at(i);
         return ((size_t)ba.x * Hv + h) * bt + ba.y;
     };
     auto Kp = [&](int i) {
-        const int2 ba = rec_at(dm, a.p, r, i);
+        const int2 ba = at(i);
         return static_cast<const InT *>(a.p.K) + (((size_t)ba.x * dm.Hk + hk) * bt + ba.y) * kD;
     };
     auto Up = [&](int i) {
-        const int2 ba = rec_at(dm, a.p, r, i);
+        const int2 ba = at(i);
         return static_cast<const UT *>(a.p.U) +
                ((((size_t)ba.x * Hv + h) * (kD / kUSub) + jr / kUSub) * bt + ba.y) * kUSub + jr % kUSub;
     };
@@ -159,6 +170,9 @@ __global__ void __launch_bounds__(kFoldThreads, RAW ? 4 : (kFoldNJ == 128 ? 2 : 
             n = (mode == 0 && occ == dm.C) ? occ : 0;
         } else if (a.kind == FK_FORCE) {
             if (mode == 1) { n = len; zero_s0 = true; } else n = occ;
+        } else if (a.kind == FK_FORK) {
+            n = a.fork_n;
+            zero_s0 = mode == 1;
         } else {  // FK_COMMIT
             int na = a.nacc[zi];
             if (na < 0 || na > a.n_draft) {
@@ -396,7 +410,7 @@ __global__ void __launch_bounds__(kFoldThreads, RAW ? 4 : (kFoldNJ == 128 ? 2 : 
     tc_fence_before();
     __syncthreads();
     if (tid == 0) {
-        bulk_s2g(state_tile, S_s, kFoldNJ * kD * 4);
+        bulk_s2g(state_out, S_s, kFoldNJ * kD * 4);
         bulk_commit();
     }
     if (warp == 0) tmem_dealloc<kFoldNJ>(tmem);
@@ -404,7 +418,7 @@ __global__ void __launch_bounds__(kFoldThreads, RAW ? 4 : (kFoldNJ == 128 ? 2 : 
     // ---- counters: last CTA of the slot resets the buffer
     if (tid == 0) {
         const int nct = gridDim.x * gridDim.y;
-        if (atomicAdd(&a.p.ticket[r], 1) == nct - 1) {
+        if (a.kind != FK_FORK && atomicAdd(&a.p.ticket[r], 1) == nct - 1) {
             a.p.ticket[r] = 0;
             a.p.occ[r] = 0;
             if (zero_s0) { a.p.mode[r] = 0; a.p.len[r] = 0; }
@@ -416,7 +430,8 @@ __global__ void __launch_bounds__(kFoldThreads, RAW ? 4 : (kFoldNJ == 128 ? 2 : 
 template <typename InT, typename UT, bool FP32_IN, int NJ, int KCM, bool RAW>
 static cudaError_t launch_fold_cfg(const FoldArgs &a, cudaStream_t s) {
     const FoldSmem L = fold_smem_layout(FP32_IN, NJ, a.kc, RAW ? a.kcap : 0);
-    auto kfn = fold_kernel<InT, UT, FP32_IN, NJ, KCM, RAW>;
+    const bool pg = a.slots || a.p.btab || a.p.sidx;
+    auto kfn = pg ? fold_kernel<InT, UT, FP32_IN, NJ, KCM, RAW, true> : fold_kernel<InT, UT, FP32_IN, NJ, KCM, RAW, false>;
     cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
     if (e != cudaSuccess) return e;
     return launch_k(kfn, dim3(kD / NJ, a.dm.Hv, a.n), dim3(kFoldThreads), L.total, s, a.pdl != 0, a);

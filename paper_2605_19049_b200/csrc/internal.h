@@ -28,6 +28,7 @@ struct Dims {
     int R, Hk, Hv, g, T, C;
     int in_dt, u_dt, keep_raw, validate;
     int bt, maxb;        // tokens per record block; blocks per slot (table row length)
+    int variant;         // 0 GDN (gate + delta rule), 1 gated LA (no delta), 2 vanilla LA
 };
 
 // Launch overlap (la_set_overlap, programmatic dependent launch): pdl = the
@@ -51,7 +52,6 @@ struct Ptrs {
 };
 
 #ifdef __CUDACC__
-__device__ __forceinline__ size_t state_of(const Ptrs &p, int r) { return p.sidx ? (size_t)p.sidx[r] : (size_t)r; }
 // (block id, offset) of record position pos of slot r
 __device__ __forceinline__ int2 rec_at(const Dims &dm, const Ptrs &p, int r, int pos) {
     if (!p.btab) return make_int2(r, pos);
@@ -93,6 +93,8 @@ enum FoldKind : int {
     FK_FULL = 0,     // chunkwise slots with occ == C
     FK_FORCE = 1,    // chunkwise slots with occ > 0; direct slots: compress, S0 = 0
     FK_COMMIT = 2,   // chunkwise: n = occ + clamp(n_acc[r], 0, n_draft)
+    FK_FORK = 3,     // state of slot `dst` <- fold of slot r's first fork_n records (S0: r's state, or 0
+                     // for a DIRECT slot); slot r and its counters untouched
 };
 
 struct FoldArgs {
@@ -108,7 +110,10 @@ struct FoldArgs {
     int raw = 0;        // mode ii: recompute u from the raw records (keep_raw) by the UT transform
     int pdl = 0, pdl_early = 0;
     const int *slots = nullptr;   // index-array batch (else first + zi)
+    int fork_n = 0, fork_dst = -1;  // FK_FORK
 };
+cudaError_t launch_commit_append(const Dims &dm, const Ptrs &p, int first, int n, const int *nacc, int n_draft,
+                                 int pdl, cudaStream_t s, int64_t *launches);
 
 struct RecArgs {
     Dims dm;

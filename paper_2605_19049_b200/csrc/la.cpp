@@ -63,6 +63,7 @@ struct la_buf {
     Ptrs p;
     int device;
     std::vector<int32_t> occ, len, mode, pending;   // host mirror
+    std::vector<uint8_t> occ_ub;                     // 1: occ is an upper bound (after la_commit_append)
     // pools: record blocks per slot, state index per slot
     // (-1: none); LIFO free stacks, back() = next id (initially ascending)
     bool paged = false, state_pool = false;
@@ -96,9 +97,9 @@ PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
     return fn;
 }
 
-// The state viewed as a 2-D fp32 tensor [R*Hv*128 rows][128], read in
-// 128-row x 32-column boxes with the 128-byte swizzle the tensor-core pass
-// of kernels (3)/prefill consumes.  Built once per handle, on first use.
+// The state viewed as a 2-D fp32 tensor [S*Hv*128 rows][128], read in
+// 32-row x 32-column boxes with the 128-byte swizzle the tensor-core state
+// passes of kernels (3)/prefill consume (conflict-free fragment reads).  Built once per handle, on first use.
 const void *state_tmap(la_buf *b) {
     if (b->tmap_state == 0) {
         b->tmap_state = 2;
@@ -106,7 +107,7 @@ const void *state_tmap(la_buf *b) {
         if (auto enc = tmap_encoder()) {
             const cuuint64_t dims[2] = {(cuuint64_t)kD, (cuuint64_t)b->sz.n_states * b->dm.Hv * kD};
             const cuuint64_t strides[1] = {(cuuint64_t)kD * 4};
-            const cuuint32_t box[2] = {32, 128};
+            const cuuint32_t box[2] = {32, 32};   // 32 columns (128 B, swizzled) x 32 rows: one d_v tile
             const cuuint32_t estr[2] = {1, 1};
             if (enc(reinterpret_cast<CUtensorMap *>(b->tmap), CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, b->p.state,
                     dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -141,7 +142,8 @@ void overlap_flags(const la_buf *b, cudaStream_t s, Args &a) {
     bool prev_wrote_mine = false;
     auto it = g_last_on_stream.find(s);
     if (it != g_last_on_stream.end()) prev_wrote_mine = it->second.wrote && it->second.state == b->p.state;
-    a.pdl_early = b->overlap && !prev_wrote_mine;
+    // (pooled handles resolve slots, states and blocks after the wait: no early loads)
+    a.pdl_early = b->overlap && !prev_wrote_mine && !b->paged && !b->state_pool;
 }
 void note_launch(const la_buf *b, cudaStream_t s, bool wrote_state) {
     LastLaunch &l = g_last_on_stream[s];
@@ -169,6 +171,7 @@ la_status check_config(const la_config *c) {
         return fail(LA_ERR_INVALID, "block_tokens must be 0 or a multiple of 4 in [4, 128]");
     if (c->block_tokens != 0 && c->n_blocks < 1) return fail(LA_ERR_INVALID, "a paged handle needs n_blocks >= 1");
     if (c->state_slots < -1) return fail(LA_ERR_INVALID, "state_slots must be >= -1");
+    if (c->variant < LA_VARIANT_GDN || c->variant > LA_VARIANT_VANILLA) return fail(LA_ERR_INVALID, "bad variant");
     return LA_OK;
 }
 
@@ -224,6 +227,12 @@ la_status check_range(la_buf *b, int32_t first, int32_t n) {
 la_status check_chunkwise(la_buf *b, int r) {
     if (b->mode[r] != LA_MODE_CHUNKWISE) return fail(LA_ERR_MODE, "slot %d is not CHUNKWISE", r);
     if (b->sidx[r] < 0) return fail(LA_ERR_MODE, "slot %d holds no state (reset it as CHUNKWISE)", r);
+    return LA_OK;
+}
+// calls that need the exact occupancy (decode, FULL flush, prefill, mixed, recurrent)
+la_status check_exact(la_buf *b, int r) {
+    if (b->occ_ub[r])
+        return fail(LA_ERR_MODE, "slot %d: occupancy known only as a bound after la_commit_append (flush FORCE first)", r);
     return LA_OK;
 }
 
@@ -487,7 +496,9 @@ la_status la_buf_create(const la_config *cfg, void *state, void *buffer, void *m
     p.occ = m; p.len = m + R; p.mode = m + 2 * R; p.ticket = m + 3 * R;
     p.status = reinterpret_cast<unsigned *>(m + 4 * R);
     b->occ.assign(R, 0); b->len.assign(R, 0); b->mode.assign(R, 0); b->pending.assign(R, 0);
+    b->occ_ub.assign(R, 0);
     dm.bt = b->sz.block_tokens; dm.maxb = b->sz.max_blocks;
+    dm.variant = cfg->variant;
     b->meta_i = m;
     b->i_sidx = b->sz.off_sidx / 4; b->i_btab = b->sz.off_btab / 4; b->i_wl = b->sz.off_wl / 4;
     b->paged = cfg->block_tokens != 0;
@@ -550,7 +561,7 @@ static la_status reset_impl(la_buf *b, int32_t first, int32_t n, int32_t mode, i
         if (e != cudaSuccess) return cuda_fail(e, "status clear");
     }
     for (int r = first; r < first + n; ++r) {
-        b->occ[r] = 0; b->len[r] = 0; b->mode[r] = mode; b->pending[r] = 0;
+        b->occ[r] = 0; b->len[r] = 0; b->mode[r] = mode; b->pending[r] = 0; b->occ_ub[r] = 0;
     }
     return LA_OK;
 }
@@ -573,7 +584,7 @@ la_status la_decode_step(la_buf *b, int32_t first, int32_t n, const void *q, con
     int j0_cap = 0;
     bool fills = false;
     for (int r = first; r < first + n; ++r) {
-        if ((st = check_chunkwise(b, r)) != LA_OK) return st;
+        if ((st = check_chunkwise(b, r)) != LA_OK || (st = check_exact(b, r)) != LA_OK) return st;
         if (b->pending[r]) return fail(LA_ERR_MODE, "slot %d has a pending verify (commit first)", r);
         if (b->occ[r] >= b->cfg.chunk) return fail(LA_ERR_CAPACITY, "slot %d buffer full (call la_flush)", r);
         j0_cap = std::max(j0_cap, b->occ[r]);
@@ -581,7 +592,8 @@ la_status la_decode_step(la_buf *b, int32_t first, int32_t n, const void *q, con
     }
     if (n == 0) return LA_OK;
     if ((st = set_device(b)) != LA_OK) return st;
-    const int fold = (b->auto_flush && fills && b->cfg.chunk <= 32) ? 1 : 0;
+    // (the fused fold is a contiguous-handle option)
+    const int fold = (b->auto_flush && fills && b->cfg.chunk <= 32 && !b->paged && !b->state_pool) ? 1 : 0;
     const std::vector<Grow> g = grow_range(b, first, n, b->occ, 1);
     if ((st = check_blocks(b, g)) != LA_OK) return st;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -608,10 +620,12 @@ la_status la_flush(la_buf *b, int32_t first, int32_t n, int32_t kind, la_stream 
     kind &= ~LA_FLUSH_RAW;
     if (kind != LA_FLUSH_FULL && kind != LA_FLUSH_FORCE) return fail(LA_ERR_INVALID, "bad flush kind");
     if (raw && !b->cfg.keep_raw) return fail(LA_ERR_INVALID, "LA_FLUSH_RAW needs a handle created with keep_raw = 1");
+    if (raw && b->cfg.variant != LA_VARIANT_GDN) return fail(LA_ERR_UNSUPPORTED, "LA_FLUSH_RAW is the GDN UT transform");
     bool any = false, all = true;
     int kcap = 0;
     for (int r = first; r < first + n; ++r) {
         if (b->pending[r]) return fail(LA_ERR_MODE, "slot %d has a pending verify (commit first)", r);
+        if (kind == LA_FLUSH_FULL && (st = check_exact(b, r)) != LA_OK) return st;
         int nr = 0;
         if (kind == LA_FLUSH_FULL)
             nr = (b->mode[r] == LA_MODE_CHUNKWISE && b->occ[r] == b->cfg.chunk) ? b->occ[r] : 0;
@@ -650,6 +664,7 @@ la_status la_flush(la_buf *b, int32_t first, int32_t n, int32_t kind, la_stream 
             if (b->mode[r] == LA_MODE_CHUNKWISE && b->occ[r] == b->cfg.chunk) b->occ[r] = 0;
         } else if (b->mode[r] == LA_MODE_CHUNKWISE) {
             b->occ[r] = 0;
+            b->occ_ub[r] = 0;
         } else if (b->len[r] > 0) {
             b->mode[r] = LA_MODE_CHUNKWISE; b->len[r] = 0; b->occ[r] = 0;
             // the compressed records are dead: keep the blocks a chunkwise buffer uses
@@ -712,7 +727,58 @@ la_status la_commit_accepted(la_buf *b, int32_t first, int32_t n, const int32_t 
     std::lock_guard<std::mutex> lk(g_enqueue_mu);
     cudaError_t e = run_fold(b, a, static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(e, "commit launch");
-    for (int r = first; r < first + n; ++r) { b->occ[r] = 0; b->pending[r] = 0; }
+    for (int r = first; r < first + n; ++r) { b->occ[r] = 0; b->pending[r] = 0; b->occ_ub[r] = 0; }
+    return LA_OK;
+}
+
+la_status la_commit_append(la_buf *b, int32_t first, int32_t n, const int32_t *n_accepted, la_stream stream) {
+    la_status st;
+    if ((st = check_handle(b)) != LA_OK || (st = check_range(b, first, n)) != LA_OK) return st;
+    if (!n_accepted) return fail(LA_ERR_INVALID, "null n_accepted");
+    if (n == 0) return LA_OK;
+    const int nd = b->pending[first];
+    int occ_max = 0;
+    for (int r = first; r < first + n; ++r) {
+        if (b->pending[r] == 0 || b->pending[r] != nd)
+            return fail(LA_ERR_MODE, "slot %d has no pending verify of %d drafts", r, nd);
+        occ_max = std::max(occ_max, b->occ[r]);
+    }
+    // append while the buffer stays within the chunk and can take another
+    // round of max_drafts drafts; else fold everything (la_commit_accepted)
+    if (occ_max + nd > b->cfg.chunk || occ_max + nd + b->cfg.max_drafts > b->sz.capacity)
+        return la_commit_accepted(b, first, n, n_accepted, stream);
+    if ((st = set_device(b)) != LA_OK) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    std::lock_guard<std::mutex> lk(g_enqueue_mu);
+    cudaError_t e = launch_commit_append(b->dm, b->p, first, n, n_accepted, nd, b->overlap, s, &b->launches);
+    if (e != cudaSuccess) return cuda_fail(e, "append-commit launch");
+    note_launch(b, s, false);
+    for (int r = first; r < first + n; ++r) { b->occ[r] += nd; b->pending[r] = 0; b->occ_ub[r] = 1; }
+    return LA_OK;
+}
+
+la_status la_state_fork(la_buf *b, int32_t src, int32_t dst, int32_t n_records, la_stream stream) {
+    la_status st;
+    if ((st = check_handle(b)) != LA_OK || (st = check_range(b, src, 1)) != LA_OK ||
+        (st = check_range(b, dst, 1)) != LA_OK)
+        return st;
+    if (src == dst) return fail(LA_ERR_INVALID, "src == dst");
+    if ((st = check_chunkwise(b, dst)) != LA_OK) return st;
+    if (b->occ[dst] != 0 || b->pending[dst] || b->occ_ub[dst])
+        return fail(LA_ERR_MODE, "slot %d: fork destination needs an empty buffer", dst);
+    if (b->occ_ub[src]) return fail(LA_ERR_MODE, "slot %d: occupancy known only as a bound", src);
+    const int have = b->mode[src] == LA_MODE_CHUNKWISE ? b->occ[src] : b->len[src];
+    if (n_records < 1 || n_records > have)
+        return fail(LA_ERR_INVALID, "n_records %d outside [1, %d] (slot %d's buffered records)", n_records, have, src);
+    if (b->mode[src] == LA_MODE_CHUNKWISE && b->sidx[src] < 0) return fail(LA_ERR_MODE, "slot %d holds no state", src);
+    if ((st = set_device(b)) != LA_OK) return st;
+    FoldArgs a;
+    a.dm = b->dm; a.p = b->p; a.first = src; a.n = 1;
+    a.kind = FK_FORK; a.nacc = nullptr; a.n_draft = 0; a.kcap = n_records; a.spec = 0;
+    a.fork_n = n_records; a.fork_dst = dst;
+    std::lock_guard<std::mutex> lk(g_enqueue_mu);
+    cudaError_t e = run_fold(b, a, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "fork launch");
     return LA_OK;
 }
 
@@ -754,7 +820,7 @@ la_status la_prefill(la_buf *b, int32_t first, int32_t n, int32_t n_tok, const v
     if ((st = check_inputs(q, k, v, alpha, beta, o, false)) != LA_OK) return st;
     if (n_tok < 0) return fail(LA_ERR_INVALID, "n_tok must be >= 0");
     for (int r = first; r < first + n; ++r) {
-        if ((st = check_chunkwise(b, r)) != LA_OK) return st;
+        if ((st = check_chunkwise(b, r)) != LA_OK || (st = check_exact(b, r)) != LA_OK) return st;
         if (b->pending[r]) return fail(LA_ERR_MODE, "slot %d has a pending verify", r);
         if (b->occ[r] != 0) return fail(LA_ERR_MODE, "slot %d: prefill needs an empty buffer (occ = %d)", r, b->occ[r]);
     }
@@ -871,6 +937,7 @@ la_status la_decode_mixed(la_buf *b, int32_t n, const int32_t *slots, const void
         if (b->pending[r]) return fail(LA_ERR_MODE, "slot %d has a pending verify (commit first)", r);
         if (b->mode[r] == LA_MODE_CHUNKWISE) {
             if (b->sidx[r] < 0) return fail(LA_ERR_MODE, "slot %d holds no state (reset it as CHUNKWISE)", r);
+            if ((st = check_exact(b, r)) != LA_OK) return st;
             if (b->occ[r] >= C) return fail(LA_ERR_CAPACITY, "slot %d buffer full (call la_flush)", r);
             j0_cw = std::max(j0_cw, b->occ[r]);
             g.push_back({r, b->occ[r] + 1});

@@ -37,6 +37,7 @@ __global__ void __launch_bounds__(256) recurrent_step_kernel(const RecArgs a) {
     float *us = bv + GR;             // u
     float *kq = us + GR;             // k . q
 
+    if (a.p.sidx && a.pdl) pdl_wait();   // state indices may come from the previous grid
     float *tiles[G];
 #pragma unroll
     for (int hh = 0; hh < G; ++hh)
@@ -80,9 +81,9 @@ __global__ void __launch_bounds__(256) recurrent_step_kernel(const RecArgs a) {
     if (tid < GR) {
         const int hh = tid / ROWS, row = tid % ROWS, h = hk * G + hh;
         const int drow = tile * ROWS + row;
-        const float al = a.alpha[(size_t)zi * Hv + h], be = a.beta[(size_t)zi * Hv + h];
+        const float al = a.dm.variant == 2 ? 1.f : a.alpha[(size_t)zi * Hv + h], be = a.beta[(size_t)zi * Hv + h];
         const float vt = to_f(static_cast<const InT *>(a.v)[((size_t)zi * Hv + h) * kD + drow]);
-        const float u = be * (vt - al * av[tid]);
+        const float u = a.dm.variant ? vt : be * (vt - al * av[tid]);   // (no delta rule: u = v)
         us[tid] = u;
         a.o[((size_t)zi * Hv + h) * kD + drow] = fmaf(al, bv[tid], u * (*kq));
     }
@@ -91,7 +92,7 @@ __global__ void __launch_bounds__(256) recurrent_step_kernel(const RecArgs a) {
     for (int rr = 0; rr < RPW; ++rr) {
         const int rf = warp * RPW + rr;
         const int h = hk * G + rf / ROWS;
-        const float al = a.alpha[(size_t)zi * Hv + h];
+        const float al = a.dm.variant == 2 ? 1.f : a.alpha[(size_t)zi * Hv + h];
         float4 *p = reinterpret_cast<float4 *>(S_s + (size_t)rf * kD) + lane;
         float4 s = *p;
         const float u = us[rf];
@@ -139,6 +140,7 @@ __global__ void __launch_bounds__(128) recurrent_verify_kernel(const RecArgs a) 
     float *be_s = al_s + 16;
     float *kqd = be_s + 16;                                          // k_t . q_t
 
+    if (a.p.sidx && a.pdl) pdl_wait();   // state indices may come from the previous grid
     const float *src = a.p.state + ((sidx_of(a.p, r) * Hv + h) * kD + (size_t)tile * ROWS) * kD;
     const uint32_t bytes = ROWS * kD * 4 + (uint32_t)N * (2 * kD + ROWS) * isz;
     if (tid == 0) {
@@ -195,8 +197,9 @@ __global__ void __launch_bounds__(128) recurrent_verify_kernel(const RecArgs a) 
             vals[2 * rr + 1] = dot4(s[rr], q4);
         }
         const float red = transposed_reduce<2 * RPW>(vals, lane);   // lane l: (row (l%16)/2, k|q = l&1)
-        const float al = al_s[t], be = be_s[t];
-        const float uk = be * (to_f(v_s[t * ROWS + warp * RPW + rl]) - al * red);   // valid on even lanes
+        const float al = a.dm.variant == 2 ? 1.f : al_s[t], be = be_s[t];
+        const float vr = to_f(v_s[t * ROWS + warp * RPW + rl]);
+        const float uk = a.dm.variant ? vr : be * (vr - al * red);   // valid on even lanes
         const float u = __shfl_sync(0xffffffffu, uk, lane & ~1);
         if (lane < 16 && (lane & 1)) {
             const size_t tok = (size_t)zi * N + t;
@@ -289,6 +292,30 @@ cudaError_t launch_recurrent_verify(const RecArgs &a, cudaStream_t s, int64_t *l
 cudaError_t launch_recurrent_commit(const RecArgs &a, cudaStream_t s, int64_t *launches) {
     if (a.n <= 0) return cudaSuccess;
     cudaError_t e = launch_k(recurrent_commit_kernel, dim3(8, a.dm.Hv, a.n), dim3(256), 0, s, a.pdl != 0, a);
+    if (e == cudaSuccess) ++*launches;
+    return e;
+}
+
+// ------------------------------------------------------------------ append commit
+// Multi-round speculation: the accepted drafts stay buffered, occ += n_acc.
+__global__ void commit_append_kernel(Ptrs p, Dims dm, int first, int n, const int *nacc, int n_draft) {
+    pdl_wait();
+    pdl_trigger();
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int na = nacc[i];
+    if (na < 0 || na > n_draft) {
+        if (dm.validate) atomicOr(p.status, 0x8u);
+        na = na < 0 ? 0 : n_draft;
+    }
+    p.occ[first + i] += na;
+}
+
+cudaError_t launch_commit_append(const Dims &dm, const Ptrs &p, int first, int n, const int *nacc, int n_draft,
+                                 int pdl, cudaStream_t s, int64_t *launches) {
+    if (n <= 0) return cudaSuccess;
+    cudaError_t e = launch_k(commit_append_kernel, dim3((n + 255) / 256), dim3(256), 0, s, pdl != 0, p, dm, first, n,
+                             nacc, n_draft);
     if (e == cudaSuccess) ++*launches;
     return e;
 }

@@ -20,6 +20,7 @@ LIB_PATH = os.environ.get("LABUF_LIB", os.path.join(_PKG, "liblabuf.so"))
 LA_OK, LA_ERR_INVALID, LA_ERR_UNSUPPORTED, LA_ERR_CAPACITY, LA_ERR_MODE, LA_ERR_CUDA, LA_ERR_NCCL = range(7)
 LA_DT_F32, LA_DT_BF16, LA_DT_F16 = 0, 1, 2
 LA_MODE_CHUNKWISE, LA_MODE_DIRECT = 0, 1
+LA_VARIANT_GDN, LA_VARIANT_GATED, LA_VARIANT_VANILLA = 0, 1, 2
 LA_FLUSH_FULL, LA_FLUSH_FORCE, LA_FLUSH_RAW = 0, 1, 2   # RAW is a flag OR-ed into FULL/FORCE (mode ii)
 STATUS_BITS = {"bad_alpha": 0x1, "bad_beta": 0x2, "nonfinite": 0x4, "bad_nacc": 0x8}
 
@@ -30,7 +31,8 @@ _STATUS_NAMES = {0: "LA_OK", 1: "LA_ERR_INVALID", 2: "LA_ERR_UNSUPPORTED", 3: "L
 EXPORTS = (
     "la_buf_query", "la_buf_create", "la_buf_destroy", "la_request_reset", "la_request_release",
     "la_decode_mixed", "la_pool_info", "la_decode_step",
-    "la_flush", "la_verify_drafts", "la_commit_accepted", "la_direct_short", "la_prefill",
+    "la_flush", "la_verify_drafts", "la_commit_accepted", "la_commit_append", "la_state_fork",
+    "la_direct_short", "la_prefill",
     "la_recurrent_step", "la_recurrent_verify", "la_recurrent_commit", "la_set_overlap", "la_set_auto_flush",
     "la_state_get", "la_state_set", "la_slot_info", "la_device_status", "la_kernel_launches", "la_last_error",
     "la_tp_unique_id", "la_tp_init", "la_tp_allgather", "la_tp_destroy",
@@ -47,7 +49,7 @@ class LaConfig(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int32) for n in (
         "max_slots", "n_qk_heads", "n_v_heads", "d_k", "d_v", "chunk", "max_drafts",
         "short_cap", "in_dtype", "u_dtype", "keep_raw", "validate", "block_tokens", "n_blocks",
-        "state_slots")]
+        "state_slots", "variant")]
 
 
 class LaSizes(ctypes.Structure):
@@ -97,6 +99,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "la_flush": [VP, I32, I32, I32, VP],
         "la_verify_drafts": [VP, I32, I32, I32, VP, VP, VP, VP, VP, VP, VP],
         "la_commit_accepted": [VP, I32, I32, VP, VP],
+        "la_commit_append": [VP, I32, I32, VP, VP],
+        "la_state_fork": [VP, I32, I32, I32, VP],
         "la_direct_short": [VP, I32, I32, I32, VP, VP, VP, VP, VP, VP, VP],
         "la_prefill": [VP, I32, I32, I32, VP, VP, VP, VP, VP, VP, VP],
         "la_recurrent_step": [VP, I32, I32, VP, VP, VP, VP, VP, VP, VP],
@@ -132,13 +136,14 @@ def _check(st: int):
 
 def make_config(max_slots, n_qk_heads=16, n_v_heads=32, chunk=16, max_drafts=0, short_cap=0,
                 in_dtype="bf16", u_dtype="f32", keep_raw=False, validate=False, d=128,
-                block_tokens=0, n_blocks=0, state_slots=0) -> LaConfig:
+                block_tokens=0, n_blocks=0, state_slots=0, variant="gdn") -> LaConfig:
     """block_tokens > 0: paged record blocks from a pool of n_blocks (P:140-144);
     state_slots > 0: a pool of that many states, -1: none, 0: one per slot."""
     dt = {"f32": LA_DT_F32, "bf16": LA_DT_BF16, "f16": LA_DT_F16}
+    var = {"gdn": LA_VARIANT_GDN, "gated": LA_VARIANT_GATED, "vanilla": LA_VARIANT_VANILLA}
     return LaConfig(max_slots, n_qk_heads, n_v_heads, d, d, chunk, max_drafts, short_cap,
                     dt[in_dtype], dt[u_dtype], int(keep_raw), int(validate), int(block_tokens),
-                    int(n_blocks), int(state_slots))
+                    int(n_blocks), int(state_slots), var[variant])
 
 
 def query(cfg: LaConfig) -> LaSizes:
@@ -302,6 +307,15 @@ class LaBuf:
         self._chk(n_accepted, torch.int32, (n_accepted.shape[0],), "n_accepted")
         _check(self.lib.la_commit_accepted(self.h, first, n_accepted.shape[0], _ptr(n_accepted),
                                            _stream()))
+
+    def commit_append(self, first, n_accepted):
+        """Multi-round speculation: keep the accepted drafts buffered (la_commit_append)."""
+        self._chk(n_accepted, torch.int32, (n_accepted.shape[0],), "n_accepted")
+        _check(self.lib.la_commit_append(self.h, first, n_accepted.shape[0], _ptr(n_accepted), _stream()))
+
+    def state_fork(self, src, dst, n_records):
+        """dst's state <- src's state after its first n_records records (la_state_fork)."""
+        _check(self.lib.la_state_fork(self.h, src, dst, n_records, _stream()))
 
     def direct_short(self, first, q, k, v, alpha, beta, o):
         n, m = q.shape[0], q.shape[1]

@@ -203,16 +203,17 @@ class MixedStack:
     def footprint_bytes(self):
         return sum(b.sizes.state_bytes + b.sizes.buffer_bytes + b.sizes.meta_bytes for b in self.layers)
 
-    def reset(self, states):
-        """states[l]: fp32 [n_long, Hv, d, d] start states of layer l's long slots
-        (slots 0..n_long-1; a fresh pool hands them states 0..n_long-1 in order)."""
+    def reset(self, fill):
+        """Long slots 0..n_long-1 CHUNKWISE (a fresh pool hands them states
+        0..n_long-1 in order), short slots DIRECT; fill(l, view) writes layer
+        l's start states into the fp32 [n_long, Hv, d, d] view in place."""
         s = self.spec
-        for b, S0 in zip(self.layers, states):
+        for l, b in enumerate(self.layers):
             b.reset(0, s.n_long, mode=L.LA_MODE_CHUNKWISE, zero_state=False)
             if s.n_short:
                 b.reset(s.n_long, s.n_short, mode=L.LA_MODE_DIRECT, zero_state=False)
             assert b.pool_info(s.n_long - 1)["slot_state"] == s.n_long - 1
-            b.state[:s.n_long].copy_(S0)
+            fill(l, b.state[:s.n_long])
 
     def warmup(self, long_tok, short_tok):
         """Ragged starting points as in GdnStack.warmup (long occupancies

@@ -53,6 +53,15 @@ def state0(seed, n_slots, n_v_heads, d=D, device="cuda"):
     return (torch.randn(n_slots, n_v_heads, d, d, generator=g, device=device) * (1.0 / (4 * d)) ** 0.5).contiguous()
 
 
+def fill_state0(out, seed):
+    """state0 written in place into `out` ([n, Hv, d, d] fp32 on the device):
+    the same distribution, no temporaries (large pools)."""
+    g = _gen(seed, out.device)
+    torch.randn(out.shape, generator=g, device=out.device, dtype=out.dtype, out=out)
+    out.mul_((1.0 / (4 * out.shape[-1])) ** 0.5)
+    return out
+
+
 def n_accepted(seed, n_slots, n_draft, p_accept=0.7, device="cuda"):
     """Accepted-prefix length per slot: first failed Bernoulli(p) trial among n_draft."""
     g = _gen(seed, device)

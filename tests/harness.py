@@ -23,8 +23,12 @@ def to_dev(x, dtype, device):
 class Oracle:
     """fp64 reference states for slots x V heads (north-star [d_v, d_k])."""
 
-    def __init__(self, S0: np.ndarray):   # [R, Hv, d, d]
+    def __init__(self, S0: np.ndarray, variant: str = "gdn"):   # [R, Hv, d, d]
+        """variant: 'gdn' (the recurrence P:362-365), 'gated' (alpha S + v k^T:
+        erase coefficient 0, write 1) or 'vanilla' (S + v k^T: alpha 1,
+        erase 0, write 1) -- the oracle's separate erase / write coefficients."""
         self.S = np.array(S0, dtype=np.float64, copy=True)
+        self.variant = variant
 
     def run(self, slots, tok, n_acc=None, want_o=True):
         """Advance `slots` by the tokens in tok (arrays [n, T, ...] from
@@ -39,8 +43,13 @@ class Oracle:
         def seq(x):   # [n,T,Hv,...] -> [n*Hv, T, ...]
             return np.ascontiguousarray(np.swapaxes(x, 1, 2).reshape((n * Hv, T) + x.shape[3:]))
         S = self.S[slots].reshape(n * Hv, d, d)
-        o, S_end = oracle.gdn_run(S, seq(qv), seq(kv), seq(tok["v"]), seq(tok["alpha"]),
-                                  seq(tok["beta"]), want_o=want_o)
+        alpha, beta_e, beta_w = seq(tok["alpha"]), seq(tok["beta"]), None
+        if self.variant != "gdn":
+            beta_e, beta_w = np.zeros_like(beta_e), np.ones_like(beta_e)
+            if self.variant == "vanilla":
+                alpha = np.ones_like(alpha)
+        o, S_end = oracle.gdn_run(S, seq(qv), seq(kv), seq(tok["v"]), alpha, beta_e, beta_w=beta_w,
+                                  want_o=want_o)
         out = None if o is None else np.swapaxes(o.reshape(n, Hv, T, d), 1, 2)
         if n_acc is None:
             self.S[slots] = S_end.reshape(n, Hv, d, d)
@@ -51,7 +60,7 @@ class Oracle:
                     continue
                 sub = {k_: v_[i:i + 1, :m] for k_, v_ in tok.items()}
                 saved = self.S[[s]].copy()
-                o2 = Oracle(saved)
+                o2 = Oracle(saved, self.variant)
                 o2.run([0], sub, want_o=False)
                 self.S[s] = o2.S[0]
         return out

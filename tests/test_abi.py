@@ -256,3 +256,18 @@ def test_state_pool_exhaustion_before_device_work(lib):
     assert lib.la_decode_mixed(h, 2, sl, ok, ok, ok, ok, ok, ok, None) == L.LA_ERR_INVALID   # out of range
     assert lib.la_kernel_launches(h) == 0
     lib.la_buf_destroy(h)
+
+
+def test_variant_field(lib):
+    """la_config.variant: GDN / gated / vanilla accepted, anything else
+    LA_ERR_INVALID; mode ii (LA_FLUSH_RAW) is the GDN UT transform only."""
+    for v in ("gdn", "gated", "vanilla"):
+        L.query(_cfg(variant=v))
+    cfg = _cfg()
+    cfg.variant = 3
+    with pytest.raises(L.LaError) as e:
+        L.query(cfg)
+    assert e.value.status == L.LA_ERR_INVALID
+    h = _fake_handle(lib, _cfg(keep_raw=True, variant="vanilla"))
+    assert lib.la_flush(h, 0, 1, L.LA_FLUSH_FULL | L.LA_FLUSH_RAW, None) == L.LA_ERR_UNSUPPORTED
+    lib.la_buf_destroy(h)
