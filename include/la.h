@@ -293,11 +293,12 @@ LA_API la_status la_direct_short(la_buf *buf, int32_t first, int32_t n, int32_t 
                           const float *alpha, const float *beta, float *o,
                           la_stream stream);
 
-/* Chunkwise prefill: folds a prompt of n_tok tokens into the state
- * of CHUNKWISE slots with occ == 0, in chunks of `chunk` tokens: each chunk
- * runs the forward-substitution kernel (the UT transform of P:395-397) and
- * the tensor-core fold.  o may be NULL; otherwise it receives the
- * prompt outputs [n][n_tok][Hv][d_v].  Leaves occ = 0. */
+/* Chunkwise prefill: folds a prompt of n_tok tokens into
+ * the state of CHUNKWISE slots with occ == 0, in chunks of P = max(chunk,
+ * min(64, T)) tokens: each chunk runs the forward-substitution kernel (the UT
+ * transform of P:395-397, state mat-vecs on the tensor cores, 16 tokens per
+ * launch) and the tensor-core fold.  o may be NULL; otherwise it
+ * receives the prompt outputs [n][n_tok][Hv][d_v].  Leaves occ = 0. */
 LA_API la_status la_prefill(la_buf *buf, int32_t first, int32_t n, int32_t n_tok,
                      const void *q, const void *k, const void *v,
                      const float *alpha, const float *beta, float *o,

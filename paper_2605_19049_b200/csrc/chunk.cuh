@@ -51,6 +51,9 @@ struct CtaLayout {
     uint32_t S, U, K, Gs, q, k, v, kq32, Ck, Cq, av, bv, Gn, Bn, Y, Kf, Bm, bar, bytes;
 };
 
+// fused fold (decode with auto-flush): A operand U~ [row][record], rows of
+// kAuS floats (conflict-free ldmatrix; records <= kFusedFoldMaxC = 32)
+constexpr int kAuS = 36;
 // warp-MMA state pass: B operand rows (k_t, q_t of the new tokens, zero padded
 // to whole n8 tiles), row stride padded to 132 floats (conflict-free
 // fragment reads); fp32 tokens keep a hi and a lo copy
@@ -82,7 +85,7 @@ __host__ __device__ inline CtaLayout cta_layout(int TPC, int nt, bool has_state,
     L.Gn = o; o = al128(o + (uint32_t)(nt * 4));
     L.Bn = o; o = al128(o + (uint32_t)(nt * 4));
     L.Y = o;  o = al128(o + (tc ? (uint32_t)(tc_nmma(nt) * kD * 4 * (isz == 4 ? 2 : 1)) : 0u));
-    L.Kf = o; o = al128(o + (fold ? (uint32_t)(J * kD * 4) : 0u));   // fused fold: fp32 keys
+    L.Kf = o; o = al128(o + (fold ? (uint32_t)(TPC * 32 * kAuS * 4) : 0u));   // fused fold: A = U~ rows
     L.Bm = o; o = al128(o + (mma ? (uint32_t)(mma_nrows(nt) * kBmStride * 4 * (isz == 4 ? 2 : 1)) : 0u));
     L.bar = o; o += 64;
     L.bytes = al128(o);
@@ -842,35 +845,70 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
         }
         if constexpr (FOLD) {
             if (J == dm.C) {   // CTA-uniform
-                // the J keys as fp32 rows, once per CTA
-                float *Kf = reinterpret_cast<float *>(smem + L.Kf);
-                for (int e = tid; e < J * kD; e += NTHR)
-                    Kf[e] = to_f(e < j0 * kD ? K_s[e] : k_s[e - j0 * kD]);
-                // this thread's state row: S_new = e^{G_t} S0 + sum_{i<J} e^{G_t-G_i} u_i k_i^T
+                // S_new = e^{G_t} S0 + U~ K,  U~[row][i] = e^{G_t-G_i} u_i[row] on the
+                // warp-level tensor cores: per warp D[32 rows x 128] = U~ [32 x J] . K [J x 128]
+                // (split TF32: U~ hi + lo; bf16 keys exact, fp32 keys hi + lo), J padded to 8
                 const float gt = Gn_s[0];
-                float coef[kFusedFoldMaxC];
+                const float eG = expf(gt);
+                float *Au = reinterpret_cast<float *>(smem + L.Kf) + (size_t)wt * 32 * kAuS;
 #pragma unroll
                 for (int i = 0; i < kFusedFoldMaxC; ++i)
-                    coef[i] = i < j0 ? expf(gt - G_s[i]) * to_f(ut[(size_t)i * kUSub]) : (i == j0 ? un[0] : 0.f);
-                const float eG = expf(gt);
-                float *Srow = const_cast<float *>(S_s) + (size_t)(wt * 32 + row) * kD;
-                __syncthreads();
-                // rotated 16-byte chunks: the lanes (rows) hit distinct bank groups of
-                // the state rows and sweep each key row once; packed FFMA2
-                for (int cc = 0; cc < kD / 4; ++cc) {
-                    const int c4 = 4 * ((cc + lane) & (kD / 4 - 1));
-                    const float4 s4 = *reinterpret_cast<const float4 *>(Srow + c4);
-                    float2 s01 = make_float2(eG * s4.x, eG * s4.y), s23 = make_float2(eG * s4.z, eG * s4.w);
+                    Au[row * kAuS + i] = i < j0 ? expf(gt - G_s[i]) * to_f(ut[(size_t)i * kUSub]) : (i == j0 ? un[0] : 0.f);
+                __syncwarp();
+                const int g = lane >> 2, t4 = lane & 3, lr = lane & 7, lm = lane >> 3;
+                const int KS = (J + 7) / 8;
+                auto key = [&](int i, int c) -> float { return i < J ? to_f(i < j0 ? K_s[i * kD + c] : k_s[c]) : 0.f; };
+                float *Sw = const_cast<float *>(S_s) + (size_t)wt * 32 * kD;
+                const uint32_t au = smem_u32(Au) + (uint32_t)(((lr + (lm & 1) * 8) * kAuS + (lm >> 1) * 4) * 4);
+#pragma unroll 1
+                for (int ng = 0; ng < kD / 32; ++ng) {
+                    float acc[2][4][4];
 #pragma unroll
-                    for (int i = 0; i < kFusedFoldMaxC; ++i) {
-                        if (i < J) {
-                            const float4 k4 = *reinterpret_cast<const float4 *>(Kf + i * kD + c4);
-                            const float2 cf = make_float2(coef[i], coef[i]);
-                            s01 = ffma2(cf, make_float2(k4.x, k4.y), s01);
-                            s23 = ffma2(cf, make_float2(k4.z, k4.w), s23);
+                    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+                        for (int nt = 0; nt < 4; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = acc[mt][nt][2] = acc[mt][nt][3] = 0.f;
+#pragma unroll 1
+                    for (int ks = 0; ks < KS; ++ks) {
+                        uint32_t ahi[2][4], alo[2][4];
+#pragma unroll
+                        for (int mt = 0; mt < 2; ++mt) {
+                            uint32_t x[4];
+                            ldsm_x4(x, au + (uint32_t)((mt * 16 * kAuS + ks * 8) * 4));
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) {
+                                const uint32_t hi = x[q] & 0xFFFFE000u;
+                                ahi[mt][q] = hi;
+                                alo[mt][q] = __float_as_uint(__uint_as_float(x[q]) - __uint_as_float(hi));
+                            }
+                        }
+#pragma unroll
+                        for (int nt = 0; nt < 4; ++nt) {
+                            const int c = ng * 32 + nt * 8 + g;
+                            const float b0 = key(ks * 8 + t4, c), b1 = key(ks * 8 + t4 + 4, c);
+                            const uint32_t h0 = __float_as_uint(b0) & 0xFFFFE000u, h1 = __float_as_uint(b1) & 0xFFFFE000u;
+#pragma unroll
+                            for (int mt = 0; mt < 2; ++mt) {
+                                mma_tf32_16x8x8(acc[mt][nt], ahi[mt], h0, h1);
+                                mma_tf32_16x8x8(acc[mt][nt], alo[mt], h0, h1);
+                                if constexpr (isz == 4)   // fp32 keys: + U~_hi . K_lo
+                                    mma_tf32_16x8x8(acc[mt][nt], ahi[mt],
+                                                    __float_as_uint(b0 - __uint_as_float(h0)),
+                                                    __float_as_uint(b1 - __uint_as_float(h1)));
+                            }
                         }
                     }
-                    *reinterpret_cast<float4 *>(Srow + c4) = make_float4(s01.x, s01.y, s23.x, s23.y);
+                    // epilogue: rows g, g + 8 of each m-tile, columns 2 t4, 2 t4 + 1
+#pragma unroll
+                    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+                        for (int nt = 0; nt < 4; ++nt) {
+                            const int c = ng * 32 + nt * 8 + 2 * t4;
+                            float2 *p0 = reinterpret_cast<float2 *>(Sw + (size_t)(mt * 16 + g) * kD + c);
+                            float2 *p1 = reinterpret_cast<float2 *>(Sw + (size_t)(mt * 16 + g + 8) * kD + c);
+                            const float2 s0 = *p0, s1 = *p1;
+                            *p0 = make_float2(fmaf(eG, s0.x, acc[mt][nt][0]), fmaf(eG, s0.y, acc[mt][nt][1]));
+                            *p1 = make_float2(fmaf(eG, s1.x, acc[mt][nt][2]), fmaf(eG, s1.y, acc[mt][nt][3]));
+                        }
                 }
             }
         }
