@@ -418,6 +418,18 @@ def main(argv=None):
         for b in bufs:
             b.flush(0, B, L.LA_FLUSH_FULL)
 
+    def cycle_in_order():
+        # the serving order: each layer's flush right after the decode that
+        # filled its buffers (eager flush, reading Z15), before the next layer
+        for t in range(C):
+            for l, b in enumerate(bufs):
+                x = inputs[t][l]
+                b.decode_step(0, x["q"], x["k"], x["v"], x["alpha"], x["beta"], x["o"])
+                if tp:
+                    comm.allgather(x["o"], gathered[l])
+                if t == C - 1:
+                    b.flush(0, B, L.LA_FLUSH_FULL)
+
     # unfused cycle (C decode launches + the tcgen05 flush kernel): measured
     # first, reported beside the headline and for the flush kernel's row
     n0 = sum(b.kernel_launches() for b in bufs)
@@ -431,6 +443,11 @@ def main(argv=None):
     uf_total_ms, (dec_ms, fl_ms) = timed_graphs(torch, stream, [g_dec, g_fl], K, W)
     uf_total_ms = max_over_ranks(uf_total_ms)
     del g_dec, g_fl
+    g_io = capture(torch, stream, cycle_in_order)
+    barrier()
+    io_total_ms, _ = timed_graphs(torch, stream, [g_io], K, W)
+    io_total_ms = max_over_ranks(io_total_ms)
+    del g_io
     auto = args.auto_flush
     # the fused flush (la_set_auto_flush): the step that fills
     # the buffers folds them inside the decode kernel; always measured (row
@@ -449,7 +466,10 @@ def main(argv=None):
     if auto:
         total_ms, launches_per_step = f_total_ms, f_launches
     else:
-        total_ms, launches_per_step = uf_total_ms, dec_launches + fl_launches
+        # the same launches in the serving order (flush after the filling
+        # decode of each layer) or phase by phase, whichever the step uses
+        total_ms, launches_per_step = min(uf_total_ms, io_total_ms), dec_launches + fl_launches
+    in_order = (not auto) and io_total_ms <= uf_total_ms
     barrier()
     t_c1 = time.time()
     total_ms = max_over_ranks(total_ms)
@@ -510,7 +530,8 @@ def main(argv=None):
                                    f"dp{world} (requests partitioned, no collective)"),
                    "step": (f"one buffer cycle: {C} decode steps, the last folding the buffer in-kernel "
                             f"(fused flush), x {NL} layer instances" if auto else
-                            f"one buffer cycle: {C} decode steps + 1 flush, x {NL} layer instances"),
+                            f"one buffer cycle: {C} decode steps + 1 flush, x {NL} layer instances"
+                            + (" (each layer's flush right after its filling decode)" if in_order else "")),
                    "fused_flush": auto,
                    "l2": f"inputs larger than L2: {NL} layers x {B * lb.st / 2**20:.0f} MiB state rotated per step",
                    "cuda_graphs": True, "launch_overlap": not args.no_overlap},
@@ -522,7 +543,11 @@ def main(argv=None):
                       "tokens_per_s_per_gpu": B / (rec_us_per_token * 1e-6),
                       "hbm_frac_of_measured": gbs(rec_bytes_per_launch, rec_us) / peak},
         "unfused": {"us_per_token": uf_us_per_token, "tokens_per_s_per_gpu": B / (uf_us_per_token * 1e-6),
-                    "note": "the cycle with the separate tcgen05 flush kernel (la_set_auto_flush 0)"},
+                    "note": "the cycle with the separate tcgen05 flush kernel (la_set_auto_flush 0), all decode "
+                            "steps of the cycle first, then the flushes (per-kernel times come from this run)"},
+        "in_order": {"us_per_token": 1e3 * io_total_ms / K / (C * NL),
+                     "note": "the same launches in the serving order: each layer's flush directly after the "
+                             "decode that filled its buffers (eager flush, reading Z15)"},
         "fused_flush": {"us_per_token": 1e3 * f_total_ms / K / (C * NL),
                         "note": "the cycle with the flush folded into the filling decode step on CUDA cores "
                                 "(la_set_auto_flush 1, SURVEY NEXT-1); slower on B200: the 64-thread decode CTA "

@@ -259,6 +259,24 @@ LA_API la_status la_verify_drafts(la_buf *buf, int32_t first, int32_t n, int32_t
 LA_API la_status la_commit_accepted(la_buf *buf, int32_t first, int32_t n,
                              const int32_t *n_accepted, la_stream stream);
 
+/* Branch (beam) candidates: n_branch candidate
+ * branches of n_draft tokens each, all extending the slot's current buffer,
+ * verified in one launch: inputs [n][n_branch * n_draft][...] branch-major;
+ * token p of branch b sees the state, the buffered records and tokens
+ * 0..p of its own branch only (the decay restarts per branch).  Records are
+ * written at occ + b * n_draft + p; nothing is folded and no per-branch state
+ * exists.  n_branch * n_draft <= min(max_drafts, 16). */
+LA_API la_status la_verify_branches(la_buf *buf, int32_t first, int32_t n, int32_t n_branch,
+                             int32_t n_draft, const void *q, const void *k, const void *v,
+                             const float *alpha, const float *beta, float *o, la_stream stream);
+
+/* Commit of the accepted branch: folds records [0, occ) and the first
+ * n_accepted[r] records of branch branch[r] (DEVICE int32 [n] each, clamped;
+ * status bit with validate = 1) into the state; occ <- 0.  LA_ERR_MODE unless
+ * the range has a pending branch verify of one shape. */
+LA_API la_status la_commit_branch(la_buf *buf, int32_t first, int32_t n, const int32_t *branch,
+                           const int32_t *n_accepted, la_stream stream);
+
 /* Multi-round buffered speculation: commit the accepted
  * prefix by APPENDING it -- the accepted drafts' records (k, u, G) are
  * already the recurrence's records (u_t depends only on tokens <= t),

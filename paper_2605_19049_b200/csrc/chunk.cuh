@@ -401,10 +401,12 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
             if (!(be_l >= 0.f && be_l <= 1.f)) bad |= 0x2u;
         }
     }
+    // (branch verify: the scan restarts at every branch of a.seg tokens)
+    const int segl = a.seg > 0 ? a.seg : NT;
 #pragma unroll
     for (int off = 1; off < NT; off <<= 1) {
         const float y = __shfl_up_sync(0xffffffffu, x_l, off);
-        if (lane >= off) x_l += y;
+        if (lane % segl >= off) x_l += y;
     }
     mbar_wait(tokb, 0);   // (non-MMA kinds: tokb == full, the state and the tokens)
     // multi-token launches read k_t / q_t once per row step: widen them to
@@ -642,7 +644,8 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
                 const float gt = __shfl_sync(0xffffffffu, gn_l, t);
                 const float gnew = __shfl_sync(0xffffffffu, gn_l, inew < NT ? inew : 0);
                 if (xid[o] >= 0 && i < J && t < n_new) {
-                    const bool valid = isq ? (i <= j0 + t) : (i < j0 + t);
+                    bool valid = isq ? (i <= j0 + t) : (i < j0 + t);
+                    if (i >= j0 && (i - j0) / segl != t / segl) valid = false;   // another branch
                     float cf = 0.f;
                     if (valid) cf = expf(gt - (i < j0 ? G_s[i] : gnew)) * res[o];
                     (isq ? Cq : Ck)[t * Jst + i] = cf;

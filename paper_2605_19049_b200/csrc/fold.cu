@@ -107,7 +107,13 @@ __global__ void __launch_bounds__(kFoldThreads, RAW ? 4 : (kFoldNJ == 128 ? 2 : 
     // this thread's delta value u_i[jr] (U is tile-major
     // [blk][Hv][d/kUSub][bt][kUSub]), log decay, raw value, beta
     // (PG: block table lookups; else the slot's own region, block = slot)
-    auto at = [&](int i) -> int2 { return PG ? rec_at(dm, a.p, r, i) : make_int2(r, i); };
+    // (FK_BRANCH: record i >= occ of the folded prefix is the accepted branch's
+    //  record occ + b n_draft + (i - occ); set once the counters are read)
+    int bocc = 1 << 30, boff = 0;
+    auto at = [&](int i) -> int2 {
+        const int ii = i >= bocc ? i + boff : i;
+        return PG ? rec_at(dm, a.p, r, ii) : make_int2(r, ii);
+    };
     auto rec = [&](int i) -> size_t {   // (block * Hv + h) * bt + offset
         const int2 ba = at(i);
         return ((size_t)ba.x * Hv + h) * bt + ba.y;
@@ -173,6 +179,16 @@ __global__ void __launch_bounds__(kFoldThreads, RAW ? 4 : (kFoldNJ == 128 ? 2 : 
         } else if (a.kind == FK_FORK) {
             n = a.fork_n;
             zero_s0 = mode == 1;
+        } else if (a.kind == FK_BRANCH) {
+            int na = a.nacc[zi], br = a.branch[zi];
+            if (na < 0 || na > a.n_draft || br < 0 || br >= a.n_branch) {
+                if (dm.validate) atomicOr(a.p.status, 0x8u);
+                na = na < 0 ? 0 : (na > a.n_draft ? a.n_draft : na);
+                br = br < 0 ? 0 : (br >= a.n_branch ? a.n_branch - 1 : br);
+            }
+            n = occ + na;
+            meta[2] = occ;
+            meta[3] = br * a.n_draft;
         } else {  // FK_COMMIT
             int na = a.nacc[zi];
             if (na < 0 || na > a.n_draft) {
@@ -214,7 +230,7 @@ __global__ void __launch_bounds__(kFoldThreads, RAW ? 4 : (kFoldNJ == 128 ? 2 : 
             for (int u = 0; u < 16; ++u) if (i0 + NPAR * u < a.kcap) Us[(i0 + NPAR * u) * kFoldNJ + jb] = t[u];
         }
         for (int i = tid; i < a.kcap; i += kFoldThreads) { Gs[i] = a.p.G[rec(i)]; Bs[i] = a.p.B[rec(i)]; }
-    } else {
+    } else if (a.kind != FK_BRANCH) {
         load_chunk(0, min(KC, a.kcap));
     }
     tc_fence_before();
@@ -222,6 +238,11 @@ __global__ void __launch_bounds__(kFoldThreads, RAW ? 4 : (kFoldNJ == 128 ? 2 : 
     tc_fence_after();
     const int n = meta[0];
     const bool zero_s0 = meta[1] != 0;
+    if (a.kind == FK_BRANCH) {   // the record remap needs the counters: load after them
+        bocc = meta[2];
+        boff = meta[3];
+        if constexpr (!RAW) load_chunk(0, min(KC, n));
+    }
     const uint32_t tmem = *tmem_slot;
     if (n == 0) {   // nothing to fold: state untouched, counters unchanged
         if (a.spec) mbar_wait(bar_ld, 0);   // the speculative copy must land before exit

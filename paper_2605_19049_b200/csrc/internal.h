@@ -74,6 +74,8 @@ struct ChunkArgs {
     int n_new;          // tokens processed per slot in this launch (<= kMaxNewPerLaunch)
     int j0_cap;         // max over the range of the buffered count j0 (sizes smem)
     int j_add;          // added to the device count (verify split into several launches)
+    int seg = 0;        // branch verify: new tokens form independent branches of `seg` tokens
+                        // (causal and cumulative decay only within a branch); 0 = one sequence
     int tok_total;      // tokens per slot in the caller's q/k/v/alpha/beta/o arrays
     int tok_offset;     // first token of this launch inside those arrays
     int kind;
@@ -93,6 +95,7 @@ enum FoldKind : int {
     FK_FULL = 0,     // chunkwise slots with occ == C
     FK_FORCE = 1,    // chunkwise slots with occ > 0; direct slots: compress, S0 = 0
     FK_COMMIT = 2,   // chunkwise: n = occ + clamp(n_acc[r], 0, n_draft)
+    FK_BRANCH = 4,   // commit of branch b: records [0, occ) + [occ + b n_draft, occ + b n_draft + n_acc)
     FK_FORK = 3,     // state of slot `dst` <- fold of slot r's first fork_n records (S0: r's state, or 0
                      // for a DIRECT slot); slot r and its counters untouched
 };
@@ -111,6 +114,8 @@ struct FoldArgs {
     int pdl = 0, pdl_early = 0;
     const int *slots = nullptr;   // index-array batch (else first + zi)
     int fork_n = 0, fork_dst = -1;  // FK_FORK
+    const int *branch = nullptr;    // FK_BRANCH: accepted branch per slot
+    int n_branch = 1;               // FK_BRANCH: branches of n_draft drafts
 };
 cudaError_t launch_commit_append(const Dims &dm, const Ptrs &p, int first, int n, const int *nacc, int n_draft,
                                  int pdl, cudaStream_t s, int64_t *launches);

@@ -64,6 +64,7 @@ struct la_buf {
     int device;
     std::vector<int32_t> occ, len, mode, pending;   // host mirror
     std::vector<uint8_t> occ_ub;                     // 1: occ is an upper bound (after la_commit_append)
+    std::vector<int32_t> branch_nd;                  // pending branch verify: drafts per branch (0: plain verify)
     // pools: record blocks per slot, state index per slot
     // (-1: none); LIFO free stacks, back() = next id (initially ascending)
     bool paged = false, state_pool = false;
@@ -265,7 +266,7 @@ la_status set_device(la_buf *b) {
 cudaError_t run_chunk(la_buf *b, int first, int n, int n_tok, int j0_cap, int tok_base, int tok_total,
                       int kind, const void *q, const void *k, const void *v, const float *alpha,
                       const float *beta, float *o, cudaStream_t s, int fold = 0,
-                      const int *slots = nullptr, const int *pos = nullptr, int passes = 3) {
+                      const int *slots = nullptr, const int *pos = nullptr, int passes = 3, int seg = 0) {
     const int mx = max_new_per_launch(b->dm.g);
     const size_t isz = dt_size(b->cfg.in_dtype);
     const size_t d = kD;
@@ -295,6 +296,7 @@ cudaError_t run_chunk(la_buf *b, int first, int n, int n_tok, int j0_cap, int to
                 a.pos = pos ? pos + s0 : nullptr;
                 a.tmap = (kind == CK_VERIFY || kind == CK_PREFILL) && m >= 2 ? state_tmap(b) : nullptr;
                 a.fold = fold;
+                a.seg = seg;
                 a.dry = pass == 0;
                 overlap_flags(b, s, a);
                 if (slots) a.pdl_early = 0;   // the slot list itself comes from a previous grid
@@ -497,6 +499,7 @@ la_status la_buf_create(const la_config *cfg, void *state, void *buffer, void *m
     p.status = reinterpret_cast<unsigned *>(m + 4 * R);
     b->occ.assign(R, 0); b->len.assign(R, 0); b->mode.assign(R, 0); b->pending.assign(R, 0);
     b->occ_ub.assign(R, 0);
+    b->branch_nd.assign(R, 0);
     dm.bt = b->sz.block_tokens; dm.maxb = b->sz.max_blocks;
     dm.variant = cfg->variant;
     b->meta_i = m;
@@ -561,7 +564,7 @@ static la_status reset_impl(la_buf *b, int32_t first, int32_t n, int32_t mode, i
         if (e != cudaSuccess) return cuda_fail(e, "status clear");
     }
     for (int r = first; r < first + n; ++r) {
-        b->occ[r] = 0; b->len[r] = 0; b->mode[r] = mode; b->pending[r] = 0; b->occ_ub[r] = 0;
+        b->occ[r] = 0; b->len[r] = 0; b->mode[r] = mode; b->pending[r] = 0; b->occ_ub[r] = 0; b->branch_nd[r] = 0;
     }
     return LA_OK;
 }
@@ -715,9 +718,11 @@ la_status la_commit_accepted(la_buf *b, int32_t first, int32_t n, const int32_t 
     if (!n_accepted) return fail(LA_ERR_INVALID, "null n_accepted");
     if (n == 0) return LA_OK;
     const int nd = b->pending[first];
-    for (int r = first; r < first + n; ++r)
+    for (int r = first; r < first + n; ++r) {
         if (b->pending[r] == 0 || b->pending[r] != nd)
             return fail(LA_ERR_MODE, "slot %d has no pending verify of %d drafts", r, nd);
+        if (b->branch_nd[r]) return fail(LA_ERR_MODE, "slot %d: a branch verify is committed by la_commit_branch", r);
+    }
     if ((st = set_device(b)) != LA_OK) return st;
     FoldArgs a;
     a.dm = b->dm; a.p = b->p; a.first = first; a.n = n;
@@ -731,6 +736,66 @@ la_status la_commit_accepted(la_buf *b, int32_t first, int32_t n, const int32_t 
     return LA_OK;
 }
 
+la_status la_verify_branches(la_buf *b, int32_t first, int32_t n, int32_t n_branch, int32_t n_draft,
+                             const void *q, const void *k, const void *v, const float *alpha, const float *beta,
+                             float *o, la_stream stream) {
+    la_status st;
+    if ((st = check_handle(b)) != LA_OK || (st = check_range(b, first, n)) != LA_OK) return st;
+    if ((st = check_inputs(q, k, v, alpha, beta, o, true)) != LA_OK) return st;
+    const int tot = n_branch * n_draft;
+    if (n_branch < 1 || n_draft < 1 || tot > b->cfg.max_drafts || tot > kMaxNewPerLaunch)
+        return fail(LA_ERR_INVALID, "n_branch x n_draft = %d x %d outside [1, min(max_drafts, 16)]", n_branch, n_draft);
+    int j0_cap = 0;
+    for (int r = first; r < first + n; ++r) {
+        if ((st = check_chunkwise(b, r)) != LA_OK) return st;
+        if (b->pending[r]) return fail(LA_ERR_MODE, "slot %d already has a pending verify", r);
+        if (b->occ[r] + tot > b->sz.capacity) return fail(LA_ERR_CAPACITY, "slot %d: occ + branches x drafts > capacity", r);
+        j0_cap = std::max(j0_cap, b->occ[r]);
+    }
+    if (n == 0) return LA_OK;
+    if ((st = set_device(b)) != LA_OK) return st;
+    const std::vector<Grow> g = grow_range(b, first, n, b->occ, tot);
+    if ((st = check_blocks(b, g)) != LA_OK) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    std::lock_guard<std::mutex> lk(g_enqueue_mu);
+    cudaError_t e = run_chunk(b, first, n, tot, j0_cap, 0, tot, CK_VERIFY, q, k, v, alpha, beta, o, s, 0,
+                              nullptr, nullptr, 1, n_draft);
+    if (e != cudaSuccess) return cuda_fail(e, "branch verify launch configuration");
+    Stage stg;
+    take_blocks(b, g, stg);
+    if ((e = run_stage(b, stg, s)) != cudaSuccess) return cuda_fail(e, "stage launch");
+    e = run_chunk(b, first, n, tot, j0_cap, 0, tot, CK_VERIFY, q, k, v, alpha, beta, o, s, 0, nullptr, nullptr, 2,
+                  n_draft);
+    if (e != cudaSuccess) return cuda_fail(e, "branch verify launch");
+    for (int r = first; r < first + n; ++r) { b->pending[r] = tot; b->branch_nd[r] = n_draft; }
+    return LA_OK;
+}
+
+la_status la_commit_branch(la_buf *b, int32_t first, int32_t n, const int32_t *branch, const int32_t *n_accepted,
+                           la_stream stream) {
+    la_status st;
+    if ((st = check_handle(b)) != LA_OK || (st = check_range(b, first, n)) != LA_OK) return st;
+    if (!branch || !n_accepted) return fail(LA_ERR_INVALID, "null branch / n_accepted");
+    if (n == 0) return LA_OK;
+    const int tot = b->pending[first], nd = b->branch_nd[first];
+    int occ_max = 0;
+    for (int r = first; r < first + n; ++r) {
+        if (!b->pending[r] || !b->branch_nd[r] || b->pending[r] != tot || b->branch_nd[r] != nd)
+            return fail(LA_ERR_MODE, "slot %d has no pending branch verify of the range's shape", r);
+        occ_max = std::max(occ_max, b->occ[r]);
+    }
+    if ((st = set_device(b)) != LA_OK) return st;
+    FoldArgs a;
+    a.dm = b->dm; a.p = b->p; a.first = first; a.n = n;
+    a.kind = FK_BRANCH; a.nacc = n_accepted; a.branch = branch; a.n_draft = nd; a.n_branch = tot / nd;
+    a.kcap = occ_max + nd; a.spec = 0;
+    std::lock_guard<std::mutex> lk(g_enqueue_mu);
+    cudaError_t e = run_fold(b, a, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "branch commit launch");
+    for (int r = first; r < first + n; ++r) { b->occ[r] = 0; b->pending[r] = 0; b->branch_nd[r] = 0; b->occ_ub[r] = 0; }
+    return LA_OK;
+}
+
 la_status la_commit_append(la_buf *b, int32_t first, int32_t n, const int32_t *n_accepted, la_stream stream) {
     la_status st;
     if ((st = check_handle(b)) != LA_OK || (st = check_range(b, first, n)) != LA_OK) return st;
@@ -739,8 +804,8 @@ la_status la_commit_append(la_buf *b, int32_t first, int32_t n, const int32_t *n
     const int nd = b->pending[first];
     int occ_max = 0;
     for (int r = first; r < first + n; ++r) {
-        if (b->pending[r] == 0 || b->pending[r] != nd)
-            return fail(LA_ERR_MODE, "slot %d has no pending verify of %d drafts", r, nd);
+        if (b->pending[r] == 0 || b->pending[r] != nd || b->branch_nd[r])
+            return fail(LA_ERR_MODE, "slot %d has no pending (non-branch) verify of %d drafts", r, nd);
         occ_max = std::max(occ_max, b->occ[r]);
     }
     // append while the buffer stays within the chunk and can take another

@@ -31,7 +31,8 @@ _STATUS_NAMES = {0: "LA_OK", 1: "LA_ERR_INVALID", 2: "LA_ERR_UNSUPPORTED", 3: "L
 EXPORTS = (
     "la_buf_query", "la_buf_create", "la_buf_destroy", "la_request_reset", "la_request_release",
     "la_decode_mixed", "la_pool_info", "la_decode_step",
-    "la_flush", "la_verify_drafts", "la_commit_accepted", "la_commit_append", "la_state_fork",
+    "la_flush", "la_verify_drafts", "la_commit_accepted", "la_verify_branches", "la_commit_branch",
+    "la_commit_append", "la_state_fork",
     "la_direct_short", "la_prefill",
     "la_recurrent_step", "la_recurrent_verify", "la_recurrent_commit", "la_set_overlap", "la_set_auto_flush",
     "la_state_get", "la_state_set", "la_slot_info", "la_device_status", "la_kernel_launches", "la_last_error",
@@ -100,6 +101,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "la_verify_drafts": [VP, I32, I32, I32, VP, VP, VP, VP, VP, VP, VP],
         "la_commit_accepted": [VP, I32, I32, VP, VP],
         "la_commit_append": [VP, I32, I32, VP, VP],
+        "la_verify_branches": [VP, I32, I32, I32, I32, VP, VP, VP, VP, VP, VP, VP],
+        "la_commit_branch": [VP, I32, I32, VP, VP, VP],
         "la_state_fork": [VP, I32, I32, I32, VP],
         "la_direct_short": [VP, I32, I32, I32, VP, VP, VP, VP, VP, VP, VP],
         "la_prefill": [VP, I32, I32, I32, VP, VP, VP, VP, VP, VP, VP],
@@ -307,6 +310,20 @@ class LaBuf:
         self._chk(n_accepted, torch.int32, (n_accepted.shape[0],), "n_accepted")
         _check(self.lib.la_commit_accepted(self.h, first, n_accepted.shape[0], _ptr(n_accepted),
                                            _stream()))
+
+    def verify_branches(self, first, n_branch, q, k, v, alpha, beta, o):
+        """n_branch candidate branches per slot, inputs [n, n_branch * n_draft, ...] branch-major."""
+        n, tot = q.shape[0], q.shape[1]
+        if tot % n_branch:
+            raise ValueError("tokens per slot must be n_branch x n_draft")
+        self._tok(n, tot, q, k, v, alpha, beta, o)
+        _check(self.lib.la_verify_branches(self.h, first, n, n_branch, tot // n_branch, _ptr(q), _ptr(k), _ptr(v),
+                                           _ptr(alpha), _ptr(beta), _ptr(o), _stream()))
+
+    def commit_branch(self, first, branch, n_accepted):
+        self._chk(branch, torch.int32, (branch.shape[0],), "branch")
+        self._chk(n_accepted, torch.int32, (branch.shape[0],), "n_accepted")
+        _check(self.lib.la_commit_branch(self.h, first, branch.shape[0], _ptr(branch), _ptr(n_accepted), _stream()))
 
     def commit_append(self, first, n_accepted):
         """Multi-round speculation: keep the accepted drafts buffered (la_commit_append)."""

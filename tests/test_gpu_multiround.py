@@ -108,3 +108,50 @@ def test_state_fork_from_prefix_and_from_kvs(cuda_device):
     assert_close(o.cpu().numpy(), r_o[:, 0], tol, "decode after the rebuild")
     with pytest.raises(L.LaError):
         buf.state_fork(2, 3, 21)                           # more records than the source holds
+
+
+@pytest.mark.parametrize("n_branch,n_draft", [(3, 4), (4, 2), (2, 8)])
+def test_branch_verify_and_commit(cuda_device, n_branch, n_draft):
+    """Beam/branch candidates: n_branch branches of n_draft tokens
+    from the same prefix (state + 3 buffered records) verified in one launch,
+    each branch's outputs equal to the recurrence over that branch alone; the
+    accepted branch's prefix is folded, the others never touch the state."""
+    rc = synth.Recipe(seed=3503 + n_branch, dist="stress", in_dtype="bf16")
+    tol = TOL["bf16"]
+    R, C = 3, 16
+    tot = n_branch * n_draft
+    cfg = L.make_config(R, HK, HV, chunk=C, max_drafts=16, validate=True)
+    buf = L.LaBuf(cfg, device=cuda_device)
+    slots = np.arange(R)
+    buf.reset(zero_state=False)
+    S0 = synth.state0(rc, slots, HV, 128, 128)
+    set_states(buf, S0, slots)
+    orc = Oracle(S0)
+    pre = synth.tokens(rc, slots, np.arange(3), HK, HV, 128)        # 3 buffered records
+    orc.run(slots, pre, want_o=False)
+    for t in range(3):
+        d = upload_tokens({k_: v_[:, t:t + 1] for k_, v_ in pre.items()}, "bf16", cuda_device, squeeze_t=True)
+        o = torch.empty(R, HV, 128, dtype=torch.float32, device=cuda_device)
+        buf.decode_step(0, d["q"], d["k"], d["v"], d["alpha"], d["beta"], o)
+    tok = synth.tokens(rc, slots, np.arange(100, 100 + tot), HK, HV, 128)   # branch-major
+    d = upload_tokens(tok, "bf16", cuda_device)
+    o = torch.empty(R, tot, HV, 128, dtype=torch.float32, device=cuda_device)
+    buf.verify_branches(0, n_branch, d["q"], d["k"], d["v"], d["alpha"], d["beta"], o)
+    got = o.cpu().numpy()
+    for bb in range(n_branch):
+        sub = {k_: v_[:, bb * n_draft:(bb + 1) * n_draft] for k_, v_ in tok.items()}
+        ref = Oracle(orc.S.copy()).run(slots, sub)
+        assert_close(got[:, bb * n_draft:(bb + 1) * n_draft], ref, tol, f"branch {bb} outputs")
+    branch = np.array([r % n_branch for r in range(R)], dtype=np.int32)
+    n_acc = synth.n_accepted(rc, slots, n_draft, round_idx=9)
+    buf.commit_branch(0, torch.from_numpy(branch).to(cuda_device), torch.from_numpy(n_acc).to(cuda_device))
+    for i, s in enumerate(slots):
+        bb = branch[i]
+        sub = {k_: v_[i:i + 1, bb * n_draft:bb * n_draft + n_acc[i]] for k_, v_ in tok.items()}
+        ref = Oracle(orc.S[[s]].copy())
+        if n_acc[i]:
+            ref.run([0], sub, want_o=False)
+        assert_close(buf.state_get(int(s)).cpu().numpy(), ref.S[0], tol, f"slot {s}: branch {bb}, {n_acc[i]} accepted")
+    assert buf.slot_info(0).occ == 0 and buf.slot_info(0).pending == 0
+    flags, _ = buf.device_status()
+    assert flags == 0
