@@ -312,11 +312,12 @@ LA_API la_status la_direct_short(la_buf *buf, int32_t first, int32_t n, int32_t 
                           la_stream stream);
 
 /* Chunkwise prefill: folds a prompt of n_tok tokens into
- * the state of CHUNKWISE slots with occ == 0, in chunks of P = max(chunk,
- * min(64, T)) tokens: each chunk runs the forward-substitution kernel (the UT
- * transform of P:395-397, state mat-vecs on the tensor cores, 16 tokens per
- * launch) and the tensor-core fold.  o may be NULL; otherwise it
- * receives the prompt outputs [n][n_tok][Hv][d_v].  Leaves occ = 0. */
+ * the state of CHUNKWISE slots with occ == 0, in chunks of P tokens (the
+ * handle's chunk, or la_set_prefill_chunk): each chunk runs the
+ * forward-substitution kernel (the UT transform of P:395-397, state mat-vecs
+ * on the tensor cores, 16 tokens per launch) and the tensor-core fold
+ * (P:407).  o may be NULL; otherwise it receives the prompt outputs
+ * [n][n_tok][Hv][d_v].  Leaves occ = 0. */
 LA_API la_status la_prefill(la_buf *buf, int32_t first, int32_t n, int32_t n_tok,
                      const void *q, const void *k, const void *v,
                      const float *alpha, const float *beta, float *o,
@@ -358,6 +359,10 @@ LA_API la_status la_recurrent_commit(la_buf *buf, int32_t first, int32_t n, int3
  * call of the handle on the same stream (put an event/sync or any la_* call
  * in between).  Default 0 (off).  LA_ERR_INVALID on enable not 0/1. */
 LA_API la_status la_set_overlap(la_buf *buf, int32_t enable);
+
+/* Prefill chunk length P of la_prefill: 0 = the handle's chunk (default),
+ * else 1 <= P <= min(64, T).  LA_ERR_INVALID otherwise. */
+LA_API la_status la_set_prefill_chunk(la_buf *buf, int32_t tokens);
 
 /* Fused flush: with enable = 1 and
  * chunk <= 32, a la_decode_step that fills a slot's buffer (occ reaches

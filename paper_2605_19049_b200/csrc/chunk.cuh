@@ -46,9 +46,11 @@ constexpr int kChunkTPC = 2;        // d_v tiles (warps) per CTA for the state k
 constexpr int kDirectTPC = 4;       // ... and for direct slots (the key rows dominate)
 
 __host__ __device__ inline uint32_t al128(uint32_t x) { return (x + 127u) & ~127u; }
+// row length of the record-major coefficient arrays Ck / Cq
+__host__ __device__ constexpr int ntp(int nt) { return nt == 1 ? 1 : (nt + 3) / 4 * 4; }
 
 struct CtaLayout {
-    uint32_t S, U, K, Gs, q, k, v, kq32, Ck, Cq, av, bv, Gn, Bn, Y, Kf, Bm, bar, bytes;
+    uint32_t S, U, K, Gs, q, k, v, kq32, Ck, Cq, av, bv, Gn, Bn, Y, Kf, Bm, Ap, Kp, bar, bytes;
 };
 
 // fused fold (decode with auto-flush): A operand U~ [row][record], rows of
@@ -58,6 +60,7 @@ constexpr int kAuS = 36;
 // to whole n8 tiles), row stride padded to 132 floats (conflict-free
 // fragment reads); fp32 tokens keep a hi and a lo copy
 constexpr int kBmStride = 132;
+constexpr int kKp = 136;   // bf16 row stride of the key-rows MMA operands (272 B)
 __host__ __device__ constexpr int mma_nrows(int nt) { return (2 * nt + 7) / 8 * 8; }
 
 // tensor-core state pass: B operand rows (k_t, q_t of every new token, zero
@@ -78,8 +81,10 @@ __host__ __device__ inline CtaLayout cta_layout(int TPC, int nt, bool has_state,
     L.k = o;  o = al128(o + (uint32_t)(nt * kD * isz));
     L.v = o;  o = al128(o + (uint32_t)(nt * TPC * 32 * isz));
     L.kq32 = o; o = al128(o + (nt > 1 && isz == 2 ? (uint32_t)(nt * 2 * kD * 4) : 0u));   // fp32 k_t, q_t
-    L.Ck = o; o = al128(o + (uint32_t)(nt * J * 4));
-    L.Cq = o; o = al128(o + (uint32_t)(nt * J * 4));
+    // Ck / Cq are record-major [i][t] (rows of ntp(nt) floats): the records sum
+    // reads all tokens' coefficients of a record with 16-byte loads
+    L.Ck = o; o = al128(o + (uint32_t)(ntp(nt) * J * 4));
+    L.Cq = o; o = al128(o + (uint32_t)(ntp(nt) * J * 4));
     L.av = o; o = al128(o + (uint32_t)(has_state ? TPC * nt * 32 * 4 : 0));
     L.bv = o; o = al128(o + (uint32_t)(has_state ? TPC * nt * 32 * 4 : 0));
     L.Gn = o; o = al128(o + (uint32_t)(nt * 4));
@@ -87,6 +92,11 @@ __host__ __device__ inline CtaLayout cta_layout(int TPC, int nt, bool has_state,
     L.Y = o;  o = al128(o + (tc ? (uint32_t)(tc_nmma(nt) * kD * 4 * (isz == 4 ? 2 : 1)) : 0u));
     L.Kf = o; o = al128(o + (fold ? (uint32_t)(TPC * 32 * kAuS * 4) : 0u));   // fused fold: A = U~ rows
     L.Bm = o; o = al128(o + (mma ? (uint32_t)(mma_nrows(nt) * kBmStride * 4 * (isz == 4 ? 2 : 1)) : 0u));
+    // key rows on the tensor cores (bf16 inputs): the 2 nt vectors and the J
+    // keys as bf16 rows padded to 272 B (conflict-free ldmatrix)
+    const bool krm = mma && isz == 2;
+    L.Ap = o; o = al128(o + (krm ? (uint32_t)(((2 * nt + 15) / 16 * 16) * kKp * 2) : 0u));
+    L.Kp = o; o = al128(o + (krm ? (uint32_t)(((J + 7) / 8 * 8) * kKp * 2) : 0u));
     L.bar = o; o += 64;
     L.bytes = al128(o);
     return L;
@@ -229,7 +239,7 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
     const int tile0 = tg * TPC;                  // first 32-row d_v tile of the CTA
     const int n_new = a.n_new;
     const bool direct = (a.kind == CK_DIRECT);
-    const int Jst = a.j0_cap + NT;               // row stride of Ck/Cq
+    constexpr int NTP = ntp(NT);                 // row stride of Ck/Cq ([record][token])
 
     extern __shared__ __align__(1024) unsigned char smem[];
     const CtaLayout L = cta_layout(TPC, NT, HAS_STATE, a.j0_cap, isz, usz, TC, FOLD, MMA);
@@ -434,6 +444,13 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
                 for (int i = 0; i < 8; ++i) x[i] = 0.f;
             }
             float4 *dst = reinterpret_cast<float4 *>(Bm + n * kBmStride + c);
+            if constexpr (isz == 2) {   // the same row in bf16 for the key-rows MMA
+                if (n < 2 * NT) {
+                    const InT *src = ((n & 1) ? q_s : k_s) + t * kD + c;
+                    *reinterpret_cast<uint4 *>(reinterpret_cast<InT *>(smem + L.Ap) + n * kKp + c) =
+                        t < n_new ? *reinterpret_cast<const uint4 *>(src) : make_uint4(0u, 0u, 0u, 0u);
+                }
+            }
             if constexpr (isz == 4) {
                 float hi[8], lo[8];
 #pragma unroll
@@ -622,6 +639,48 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
         }
         // key rows, shared out over the warps in steps of 8
         const int KS = (J + 7) / 8;
+        if constexpr (MMA && isz == 2) {
+            // on the tensor cores: raw dots D[v][i] = vec_v . key_i (v = 2t: k_t, 2t+1:
+            // q_t) = Ap [2NT x 128] . Kp^T, mma.sync m16n8k16 bf16 (products exact, fp32
+            // accumulate); keys = the j0 records then the new tokens' keys
+            constexpr int NW = TPC * WPT, MT2 = (2 * NT + 15) / 16;
+            InT *Kp = reinterpret_cast<InT *>(smem + L.Kp);
+            for (int e = tid; e < KS * 8 * (kD / 8); e += NTHR) {
+                const int i = e >> 4, c = (e & 15) * 8;
+                uint4 x = make_uint4(0u, 0u, 0u, 0u);
+                if (i < J) x = *reinterpret_cast<const uint4 *>((i < j0 ? K_s + (size_t)i * kD : k_s + (size_t)(i - j0) * kD) + c);
+                *reinterpret_cast<uint4 *>(Kp + i * kKp + c) = x;
+            }
+            __syncthreads();   // Kp, Gn_s (and Ap, written with Bm) visible
+            const int g = lane >> 2, t4 = lane & 3, lr = lane & 7, lm = lane >> 3;
+            const uint32_t ap = smem_u32(smem + L.Ap) + (uint32_t)(((lr + (lm & 1) * 8) * kKp + (lm >> 1) * 8) * 2);
+            const uint32_t kp = smem_u32(Kp) + (uint32_t)((lr * kKp + (lm & 1) * 8) * 2);
+            for (int nt = warp; nt < KS; nt += NW) {
+#pragma unroll
+                for (int mt = 0; mt < MT2; ++mt) {
+                    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+                    for (int kk = 0; kk < kD / 16; ++kk) {
+                        uint32_t av4[4], bv2[2];
+                        ldsm_x4(av4, ap + (uint32_t)((mt * 16 * kKp + kk * 16) * 2));
+                        ldsm_x2(bv2, kp + (uint32_t)((nt * 8 * kKp + kk * 16) * 2));
+                        mma_bf16_16x8x16(acc, av4, bv2[0], bv2[1]);
+                    }
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const int v = mt * 16 + g + (q >> 1) * 8, i = nt * 8 + 2 * t4 + (q & 1);
+                        const int t = v >> 1;
+                        const bool isq = v & 1;
+                        if (t < n_new && i < J) {
+                            bool valid = isq ? (i <= j0 + t) : (i < j0 + t);
+                            if (i >= j0 && (i - j0) / segl != t / segl) valid = false;   // another branch
+                            const float cf = valid ? expf(Gn_s[t] - (i < j0 ? G_s[i] : Gn_s[i - j0])) * acc[q] : 0.f;
+                            (isq ? Cq : Ck)[i * NTP + t] = cf;
+                        }
+                    }
+                }
+            }
+        } else
         for (int ks = warp; ks < KS; ks += TPC * WPT) {
             const int i = ks * 8 + team;
             float4 x[8];
@@ -648,7 +707,7 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
                     if (i >= j0 && (i - j0) / segl != t / segl) valid = false;   // another branch
                     float cf = 0.f;
                     if (valid) cf = expf(gt - (i < j0 ? G_s[i] : gnew)) * res[o];
-                    (isq ? Cq : Ck)[t * Jst + i] = cf;
+                    (isq ? Cq : Ck)[i * NTP + t] = cf;
                 }
             }
         }
@@ -787,25 +846,54 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
             return make_int2(__ldcg(a.p.btab + (size_t)r * dm.maxb + (j0 + t) / dm.bt), (j0 + t) % dm.bt);
         };
         float un[NT];
+        // records part of every token's sums, record-outer for several tokens:
+        // each u_i is loaded once and the tokens' coefficients of record i come
+        // in 16-byte loads
+        float rk[NT], rq[NT];
+        if constexpr (NT > 1) {
+#pragma unroll
+            for (int t = 0; t < NT; ++t) rk[t] = rq[t] = 0.f;
+            for (int i = sub; i < j0; i += WPT) {
+                const float u0 = to_f(ut[(size_t)i * kUSub]);
+#pragma unroll
+                for (int tc = 0; tc < NTP / 4; ++tc) {
+                    const float4 c4 = *reinterpret_cast<const float4 *>(Ck + i * NTP + 4 * tc);
+                    const float4 d4 = *reinterpret_cast<const float4 *>(Cq + i * NTP + 4 * tc);
+                    const float cv[4] = {c4.x, c4.y, c4.z, c4.w}, dv4[4] = {d4.x, d4.y, d4.z, d4.w};
+#pragma unroll
+                    for (int x = 0; x < 4; ++x) {
+                        if (4 * tc + x < NT) {
+                            rk[4 * tc + x] = fmaf(cv[x], u0, rk[4 * tc + x]);
+                            rq[4 * tc + x] = fmaf(dv4[x], u0, rq[4 * tc + x]);
+                        }
+                    }
+                }
+            }
+        }
 #pragma unroll
         for (int t = 0; t < NT; ++t) {
             if (t < n_new) {
-                const float *ck = Ck + t * Jst;
-                const float *cq = Cq + t * Jst;
+                const float *ck = Ck + t;   // coefficient of record i: ck[i * NTP]
+                const float *cq = Cq + t;
                 float ak0 = 0.f, ak1 = 0.f, aq0 = 0.f, aq1 = 0.f;
-                int i = sub;
-                for (; i + WPT < j0; i += 2 * WPT) {
-                    const float u0 = to_f(ut[(size_t)i * kUSub]);
-                    const float u1 = to_f(ut[(size_t)(i + WPT) * kUSub]);
-                    ak0 = fmaf(ck[i], u0, ak0);
-                    aq0 = fmaf(cq[i], u0, aq0);
-                    ak1 = fmaf(ck[i + WPT], u1, ak1);
-                    aq1 = fmaf(cq[i + WPT], u1, aq1);
-                }
-                if (i < j0) {
-                    const float u0 = to_f(ut[(size_t)i * kUSub]);
-                    ak0 = fmaf(ck[i], u0, ak0);
-                    aq0 = fmaf(cq[i], u0, aq0);
+                if constexpr (NT == 1) {
+                    int i = sub;
+                    for (; i + WPT < j0; i += 2 * WPT) {
+                        const float u0 = to_f(ut[(size_t)i * kUSub]);
+                        const float u1 = to_f(ut[(size_t)(i + WPT) * kUSub]);
+                        ak0 = fmaf(ck[i], u0, ak0);
+                        aq0 = fmaf(cq[i], u0, aq0);
+                        ak1 = fmaf(ck[i + WPT], u1, ak1);
+                        aq1 = fmaf(cq[i + WPT], u1, aq1);
+                    }
+                    if (i < j0) {
+                        const float u0 = to_f(ut[(size_t)i * kUSub]);
+                        ak0 = fmaf(ck[i], u0, ak0);
+                        aq0 = fmaf(cq[i], u0, aq0);
+                    }
+                } else {
+                    ak0 = rk[t];
+                    aq0 = rq[t];
                 }
                 float acc_k = ak0 + ak1, acc_q = aq0 + aq1;
 #pragma unroll
@@ -815,8 +903,8 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
                 }
 #pragma unroll
                 for (int tp = 0; tp < t; ++tp) {
-                    acc_k = fmaf(ck[j0 + tp], un[tp], acc_k);
-                    acc_q = fmaf(cq[j0 + tp], un[tp], acc_q);
+                    acc_k = fmaf(ck[(j0 + tp) * NTP], un[tp], acc_k);
+                    acc_q = fmaf(cq[(j0 + tp) * NTP], un[tp], acc_q);
                 }
                 const float vt = to_f(v_s[t * TPC * 32 + wt * 32 + row]);
                 const float bt = Bn_s[t];
@@ -832,7 +920,7 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
                 if (dm.variant != 0) u = vt;   // no delta rule: the buffered value is v_t itself
                 const UT us = from_f<UT>(u);
                 un[t] = to_f(us);                      // the stored (rounded) value
-                o = fmaf(cq[j0 + t], un[t], o);
+                o = fmaf(cq[(j0 + t) * NTP], un[t], o);
                 if (sub == 0) {
                     if (dm.validate && !isfinite(vt)) bad |= 0x4u;
                     if (a.o) a.o[(tok_of(t) * Hv + h) * kD + drow] = o;

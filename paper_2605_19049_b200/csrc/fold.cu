@@ -28,6 +28,7 @@
 namespace labuf {
 
 constexpr int kFoldKCMax = 16;   // tokens per MMA staging chunk (max)
+constexpr int kKs = 132;         // mode ii: fp32 key rows padded to 132 floats (conflict-free ldmatrix)
 constexpr int kFoldThreads = 128;
 
 struct FoldSmem {
@@ -44,7 +45,7 @@ __host__ __device__ inline FoldSmem fold_smem_layout(bool fp32_in, int nj, int k
     L.Bhi = o; o += (uint32_t)nj * kc * 4;
     L.Blo = o; o += (uint32_t)nj * kc * 4;
     L.bar = o; o += 64;
-    L.Ks = o;  o += (uint32_t)((raw_n + 15) & ~15) * kD * 4;   // rows past raw_n are zero
+    L.Ks = o;  o += (uint32_t)((raw_n + 15) & ~15) * kKs * 4;   // rows past raw_n are zero
     L.Gm = o;  o += (uint32_t)raw_n * raw_n * 4;
     L.Us = o;  o += (uint32_t)raw_n * nj * 4;
     L.Gs = o;  o += (uint32_t)raw_n * 4;
@@ -71,6 +72,7 @@ __device__ __forceinline__ uint32_t kmaj_off(int row, int k, int kc) {
 template <typename InT, typename UT, bool FP32_IN, int kFoldNJ, int KCM, bool RAW, bool PG>
 __global__ void __launch_bounds__(kFoldThreads, RAW ? 4 : (kFoldNJ == 128 ? 2 : (kFoldNJ == 32 && KCM == 16 ? 8 : 4))) fold_kernel(const FoldArgs a) {
     constexpr int NPAR = kFoldThreads / kFoldNJ;   // token parities per B row
+    static_assert(!RAW || kFoldNJ == 32, "mode ii: 4 warps x 8 d_v rows (one MMA n-tile each)");
     const int jh = blockIdx.x, h = blockIdx.y, zi = blockIdx.z;
     if constexpr (PG) {   // slot lists, state indices and block tables may come from the previous grid
         if (a.pdl) pdl_wait();
@@ -135,7 +137,7 @@ __global__ void __launch_bounds__(kFoldThreads, RAW ? 4 : (kFoldNJ == 128 ? 2 : 
 #pragma unroll
         for (int i = 0; i < KCM; ++i) {
             if constexpr (RAW)
-                kv[i] = (i < kn) ? reinterpret_cast<const float *>(smem + L.Ks)[(kc0 + i) * kD + c] : 0.f;
+                kv[i] = (i < kn) ? reinterpret_cast<const float *>(smem + L.Ks)[(kc0 + i) * kKs + c] : 0.f;
             else
                 kv[i] = (i < kn) ? to_f(Kp(kc0 + i)[c]) : 0.f;
         }
@@ -217,7 +219,7 @@ __global__ void __launch_bounds__(kFoldThreads, RAW ? 4 : (kFoldNJ == 128 ? 2 : 
 #pragma unroll
             for (int u = 0; u < 16; ++u) t[u] = (i0 + u < a.kcap) ? to_f(Kp(i0 + u)[c]) : 0.f;
 #pragma unroll
-            for (int u = 0; u < 16; ++u) Ks[(i0 + u) * kD + c] = t[u];
+            for (int u = 0; u < 16; ++u) Ks[(i0 + u) * kKs + c] = t[u];
         }
         for (int i0 = ip; i0 < a.kcap; i0 += 16 * NPAR) {
             float t[16];
@@ -270,46 +272,58 @@ __global__ void __launch_bounds__(kFoldThreads, RAW ? 4 : (kFoldNJ == 128 ? 2 : 
 #pragma unroll 8
                 for (int cc = 0; cc < kD / 4; cc += 2) {
                     const int c0 = (cc + lane) & (kD / 4 - 1), c1 = (cc + 1 + lane) & (kD / 4 - 1);
-                    const float4 x0 = *reinterpret_cast<const float4 *>(Ks + i * kD + 4 * c0);
-                    const float4 y0 = *reinterpret_cast<const float4 *>(Ks + l * kD + 4 * c0);
-                    const float4 x1 = *reinterpret_cast<const float4 *>(Ks + i * kD + 4 * c1);
-                    const float4 y1 = *reinterpret_cast<const float4 *>(Ks + l * kD + 4 * c1);
+                    const float4 x0 = *reinterpret_cast<const float4 *>(Ks + i * kKs + 4 * c0);
+                    const float4 y0 = *reinterpret_cast<const float4 *>(Ks + l * kKs + 4 * c0);
+                    const float4 x1 = *reinterpret_cast<const float4 *>(Ks + i * kKs + 4 * c1);
+                    const float4 y1 = *reinterpret_cast<const float4 *>(Ks + l * kKs + 4 * c1);
                     acc0 = fmaf(x0.x, y0.x, fmaf(x0.y, y0.y, fmaf(x0.z, y0.z, fmaf(x0.w, y0.w, acc0))));
                     acc1 = fmaf(x1.x, y1.x, fmaf(x1.y, y1.y, fmaf(x1.z, y1.z, fmaf(x1.w, y1.w, acc1))));
                 }
                 Gm[i * n + l] = Bs[i] * expf(Gs[i] - Gs[l]) * (acc0 + acc1);
             }
         }
-        // (2) right-hand side  Us[i][j] = beta_i (v_i[j] - e^{G_i} (S0 k_i)[j]); thread (jb, ip),
-        //     4 tokens per pass so each state chunk read serves 4 dot products;
-        //     rotated 16-byte chunks: the lanes (rows jb) hit distinct bank groups
-        if (!zero_s0) mbar_wait(bar_ld, 0);
-        for (int i0 = ip; i0 < n; i0 += 4 * NPAR) {
-            // tokens i0 + NPAR u (u < 4): key rows at a constant 4 x 512 B stride
-            // (rows past kcap are zero), so one rotated chunk offset addresses all five loads
-            float w[4] = {0.f, 0.f, 0.f, 0.f};
-            if (!zero_s0) {
-                const char *srow = reinterpret_cast<const char *>(S_s + jb * kD);
-                const char *krow = reinterpret_cast<const char *>(Ks + i0 * kD);
-#pragma unroll 8
-                for (int cc = 0; cc < kD / 4; ++cc) {
-                    const int off = ((cc + jb) & (kD / 4 - 1)) * 16;
-                    const float4 sv = *reinterpret_cast<const float4 *>(srow + off);
+        // (2) right-hand side  Us[i][j] = beta_i (v_i[j] - e^{G_i} W[i][j]),  W = K S0^T on the
+        //     warp-level tensor cores: W^T tile [16 tokens x 8 rows] per (m-tile, warp) =
+        //     K [tokens x 128] . S0^T [128 x rows] (mma.sync m16n8k8 tf32; bf16 keys exact,
+        //     S0 split hi + lo; fp32 keys split too); A = the padded key rows by ldmatrix
+        if (!zero_s0) {
+            mbar_wait(bar_ld, 0);
+            const int g = lane >> 2, t4 = lane & 3, lr = lane & 7, lm = lane >> 3;
+            const float *srow = S_s + (size_t)(warp * 8 + g) * kD;     // B: S0 row 8 warp + g
+            for (int mt = 0; mt < (n + 15) / 16; ++mt) {
+                float acc[4] = {0.f, 0.f, 0.f, 0.f};
+                const uint32_t ab = smem_u32(Ks) + (uint32_t)(((mt * 16 + lr + (lm & 1) * 8) * kKs + (lm >> 1) * 4) * 4);
+#pragma unroll 4
+                for (int kk = 0; kk < kD / 8; ++kk) {
+                    uint32_t ka[4];
+                    ldsm_x4(ka, ab + kk * 32);
+                    const float s0 = srow[kk * 8 + t4], s1 = srow[kk * 8 + t4 + 4];
+                    const uint32_t h0 = __float_as_uint(s0) & 0xFFFFE000u, h1 = __float_as_uint(s1) & 0xFFFFE000u;
+                    const uint32_t l0 = __float_as_uint(s0 - __uint_as_float(h0));
+                    const uint32_t l1 = __float_as_uint(s1 - __uint_as_float(h1));
+                    if constexpr (FP32_IN) {
+                        uint32_t khi[4], klo[4];
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        const float4 kv4 = *reinterpret_cast<const float4 *>(krow + off + u * NPAR * kD * 4);
-                        w[u] = fmaf(sv.x, kv4.x, w[u]);
-                        w[u] = fmaf(sv.y, kv4.y, w[u]);
-                        w[u] = fmaf(sv.z, kv4.z, w[u]);
-                        w[u] = fmaf(sv.w, kv4.w, w[u]);
+                        for (int q = 0; q < 4; ++q) {
+                            khi[q] = ka[q] & 0xFFFFE000u;
+                            klo[q] = __float_as_uint(__uint_as_float(ka[q]) - __uint_as_float(khi[q]));
+                        }
+                        mma_tf32_16x8x8(acc, khi, h0, h1);
+                        mma_tf32_16x8x8(acc, khi, l0, l1);
+                        mma_tf32_16x8x8(acc, klo, h0, h1);
+                    } else {
+                        mma_tf32_16x8x8(acc, ka, h0, h1);   // bf16 keys are exact in tf32
+                        mma_tf32_16x8x8(acc, ka, l0, l1);
                     }
                 }
-            }
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int i = i0 + NPAR * u;
-                if (i < n) Us[i * kFoldNJ + jb] = Bs[i] * (Us[i * kFoldNJ + jb] - expf(Gs[i]) * w[u]);
+                for (int q = 0; q < 4; ++q) {
+                    const int i = mt * 16 + g + (q >> 1) * 8, j = warp * 8 + 2 * t4 + (q & 1);
+                    if (i < n) Us[i * kFoldNJ + j] = Bs[i] * (Us[i * kFoldNJ + j] - expf(Gs[i]) * acc[q]);
+                }
             }
+        } else {   // compression: S0 = 0, W = 0
+            for (int i = ip; i < n; i += NPAR) Us[i * kFoldNJ + jb] = Bs[i] * Us[i * kFoldNJ + jb];
         }
         __syncthreads();
         // (3) forward substitution down each column (lane = d_v row of the tile);

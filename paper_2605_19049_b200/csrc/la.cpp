@@ -77,6 +77,7 @@ struct la_buf {
     int64_t launches = 0;
     int overlap = 0;                                 // la_set_overlap
     int auto_flush = 0;                              // la_set_auto_flush
+    int prefill_chunk = 0;                           // la_set_prefill_chunk (0: chunk)
     alignas(64) unsigned char tmap[128];             // CUtensorMap of the state (tensor-core pass)
     int tmap_state = 0;                              // 0 not built, 1 ok, 2 unavailable
 };
@@ -892,11 +893,12 @@ la_status la_prefill(la_buf *b, int32_t first, int32_t n, int32_t n_tok, const v
     if (n == 0 || n_tok == 0) return LA_OK;
     if ((st = set_device(b)) != LA_OK) return st;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    // prefill chunk: up to 64 tokens (the buffer capacity T permitting) per
-    // fold -- each 16-token launch of the chunk kernel reads S0 once, the fold
-    // reads it once and writes it once, so longer chunks cut state traffic
-    // (64-token chunks: 6 state passes per 64 tokens instead of 12 with 16)
-    const int C = std::max(b->cfg.chunk, std::min(64, b->sz.capacity));
+    // prefill chunk (la_set_prefill_chunk; default the handle's C): longer
+    // chunks cut state traffic (64 tokens: 6 state passes per 64 tokens
+    // instead of 12 with 16) but the later 16-token launches of a chunk carry
+    // the chunk's earlier records (key rows, records sum) -- measured slower
+    // at 64 with this kernel
+    const int C = b->prefill_chunk ? b->prefill_chunk : b->cfg.chunk;
     const std::vector<Grow> g = grow_range(b, first, n, b->occ, std::min(C, n_tok));
     if ((st = check_blocks(b, g)) != LA_OK) return st;
     std::lock_guard<std::mutex> lk(g_enqueue_mu);
@@ -1110,6 +1112,15 @@ la_status la_set_auto_flush(la_buf *b, int32_t enable) {
     if ((st = check_handle(b)) != LA_OK) return st;
     if (enable != 0 && enable != 1) return fail(LA_ERR_INVALID, "enable must be 0 or 1");
     b->auto_flush = enable;
+    return LA_OK;
+}
+
+la_status la_set_prefill_chunk(la_buf *b, int32_t tokens) {
+    la_status st;
+    if ((st = check_handle(b)) != LA_OK) return st;
+    if (tokens != 0 && (tokens < 1 || tokens > std::min(64, (int)b->sz.capacity)))
+        return fail(LA_ERR_INVALID, "prefill chunk %d outside [1, min(64, T = %d)] (0: chunk)", tokens, b->sz.capacity);
+    b->prefill_chunk = tokens;
     return LA_OK;
 }
 

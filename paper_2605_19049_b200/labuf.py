@@ -34,7 +34,8 @@ EXPORTS = (
     "la_flush", "la_verify_drafts", "la_commit_accepted", "la_verify_branches", "la_commit_branch",
     "la_commit_append", "la_state_fork",
     "la_direct_short", "la_prefill",
-    "la_recurrent_step", "la_recurrent_verify", "la_recurrent_commit", "la_set_overlap", "la_set_auto_flush",
+    "la_recurrent_step", "la_recurrent_verify", "la_recurrent_commit", "la_set_overlap", "la_set_prefill_chunk",
+    "la_set_auto_flush",
     "la_state_get", "la_state_set", "la_slot_info", "la_device_status", "la_kernel_launches", "la_last_error",
     "la_tp_unique_id", "la_tp_init", "la_tp_allgather", "la_tp_destroy",
 )
@@ -110,6 +111,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "la_recurrent_verify": [VP, I32, I32, I32, VP, VP, VP, VP, VP, VP, VP, VP],
         "la_recurrent_commit": [VP, I32, I32, I32, VP, VP, VP],
         "la_set_overlap": [VP, I32],
+        "la_set_prefill_chunk": [VP, I32],
         "la_set_auto_flush": [VP, I32],
         "la_state_get": [VP, I32, VP, VP],
         "la_state_set": [VP, I32, VP, VP],
@@ -370,6 +372,10 @@ class LaBuf:
     def set_overlap(self, enable=True):
         """Programmatic dependent launch for this handle's kernels (la_set_overlap)."""
         _check(self.lib.la_set_overlap(self.h, 1 if enable else 0))
+
+    def set_prefill_chunk(self, tokens=0):
+        """Prefill chunk length (la_set_prefill_chunk; 0 = the handle's chunk)."""
+        _check(self.lib.la_set_prefill_chunk(self.h, int(tokens)))
 
     def set_auto_flush(self, enable=True):
         """Fold a slot's buffer inside the decode step that fills it (la_set_auto_flush)."""

@@ -15,15 +15,17 @@ pytestmark = pytest.mark.gpu
 HK, HV = 16, 32
 
 
-@pytest.mark.parametrize("in_dtype,n_tok,short_cap,drafts", [("bf16", 300, 64, 0), ("f32", 150, 64, 0),
-                                                              ("bf16", 77, 0, 4), ("bf16", 129, 128, 0)])
-def test_long_prompt_prefill(cuda_device, in_dtype, n_tok, short_cap, drafts):
+@pytest.mark.parametrize("in_dtype,n_tok,short_cap,drafts,pc", [
+    ("bf16", 300, 64, 0, 64), ("f32", 150, 64, 0, 64), ("bf16", 77, 0, 4, 0), ("bf16", 129, 128, 0, 48),
+    ("bf16", 200, 64, 0, 0), ("f32", 70, 0, 0, 0)])
+def test_long_prompt_prefill(cuda_device, in_dtype, n_tok, short_cap, drafts, pc):
     rc = synth.Recipe(seed=3601 + n_tok, dist="stress", in_dtype=in_dtype)
     tol = TOL[in_dtype]
     R = 3
     cfg = L.make_config(R, HK, HV, chunk=16, max_drafts=drafts, short_cap=short_cap, in_dtype=in_dtype,
                         validate=True)
     buf = L.LaBuf(cfg, device=cuda_device)
+    buf.set_prefill_chunk(pc)                       # 0: the handle's chunk (16)
     slots = np.arange(R)
     buf.reset(zero_state=False)
     S0 = synth.state0(rc, slots, HV, 128, 128)
