@@ -43,6 +43,8 @@
 namespace labuf {
 
 constexpr int kChunkTPC = 2;        // d_v tiles (warps) per CTA for the state kinds
+constexpr int kMmaWPT = 1;          // warps per d_v tile for the multi-token (warp-MMA) kinds (2: measured
+                                    // slower for verify: N = 4 163 -> 176 us, N = 8 265 -> 293 us)
 constexpr int kDirectTPC = 4;       // ... and for direct slots (the key rows dominate)
 
 __host__ __device__ inline uint32_t al128(uint32_t x) { return (x + 127u) & ~127u; }
@@ -91,7 +93,8 @@ __host__ __device__ inline CtaLayout cta_layout(int TPC, int nt, bool has_state,
     L.Bn = o; o = al128(o + (uint32_t)(nt * 4));
     L.Y = o;  o = al128(o + (tc ? (uint32_t)(tc_nmma(nt) * kD * 4 * (isz == 4 ? 2 : 1)) : 0u));
     L.Kf = o; o = al128(o + (fold ? (uint32_t)(TPC * 32 * kAuS * 4) : 0u));   // fused fold: A = U~ rows
-    L.Bm = o; o = al128(o + (mma ? (uint32_t)(mma_nrows(nt) * kBmStride * 4 * (isz == 4 ? 2 : 1)) : 0u));
+    // (fp32 tokens only: bf16 tokens feed the state pass from the bf16 rows Ap)
+    L.Bm = o; o = al128(o + (mma && isz == 4 ? (uint32_t)(mma_nrows(nt) * kBmStride * 4 * 2) : 0u));
     // key rows on the tensor cores (bf16 inputs): the 2 nt vectors and the J
     // keys as bf16 rows padded to 272 B (conflict-free ldmatrix)
     const bool krm = mma && isz == 2;
@@ -208,7 +211,8 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
                                                                         const __grid_constant__ CUtensorMap tmap) {
     static_assert(!TC || (HAS_STATE && TPC == 4 && WPT == 1), "tensor-core pass: whole head per CTA");
     static_assert(!FOLD || (NT == 1 && HAS_STATE && WPT == 1 && !TC), "fused fold: decode kind only");
-    static_assert(!MMA || (HAS_STATE && WPT == 1 && NT >= 2 && !TC && !FOLD), "warp-MMA pass: multi-token state kinds");
+    static_assert(!MMA || (HAS_STATE && (WPT == 1 || WPT == 2) && NT >= 2 && !TC && !FOLD),
+                  "warp-MMA pass: multi-token state kinds");
     constexpr int NMMA = tc_nmma(NT);
     constexpr int NTHR = TPC * WPT * 32;
     constexpr int RPW = 32 / WPT;                // d_v rows per warp
@@ -444,14 +448,13 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
                 for (int i = 0; i < 8; ++i) x[i] = 0.f;
             }
             float4 *dst = reinterpret_cast<float4 *>(Bm + n * kBmStride + c);
-            if constexpr (isz == 2) {   // the same row in bf16 for the key-rows MMA
+            if constexpr (isz == 2) {   // bf16 tokens: the padded bf16 rows serve both MMA passes
                 if (n < 2 * NT) {
                     const InT *src = ((n & 1) ? q_s : k_s) + t * kD + c;
                     *reinterpret_cast<uint4 *>(reinterpret_cast<InT *>(smem + L.Ap) + n * kKp + c) =
                         t < n_new ? *reinterpret_cast<const uint4 *>(src) : make_uint4(0u, 0u, 0u, 0u);
                 }
-            }
-            if constexpr (isz == 4) {
+            } else {
                 float hi[8], lo[8];
 #pragma unroll
                 for (int i = 0; i < 8; ++i) { hi[i] = trunc_tf32(x[i]); lo[i] = x[i] - hi[i]; }
@@ -460,9 +463,6 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
                 float4 *dl = reinterpret_cast<float4 *>(Bm + (NB + n) * kBmStride + c);
                 dl[0] = make_float4(lo[0], lo[1], lo[2], lo[3]);
                 dl[1] = make_float4(lo[4], lo[5], lo[6], lo[7]);
-            } else {   // bf16 values are exact in tf32
-                dst[0] = make_float4(x[0], x[1], x[2], x[3]);
-                dst[1] = make_float4(x[4], x[5], x[6], x[7]);
             }
         }
     }
@@ -720,10 +720,11 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
         // free), split TF32: S0 = hi + lo (hi = top 19 bits), 2 passes for
         // bf16 tokens (exact in tf32), 3 for fp32 tokens (+ hi . B_lo)
         constexpr int NB = mma_nrows(NT), NJ = NB / 8;
+        constexpr int MTW = 2 / WPT;                 // m16 tiles of the 32-row tile per warp
         const int g = lane >> 2, t4 = lane & 3;
-        float acc[2][NJ][4];
+        float acc[MTW][NJ][4];
 #pragma unroll
-        for (int mt = 0; mt < 2; ++mt)
+        for (int mt = 0; mt < MTW; ++mt)
 #pragma unroll
             for (int j = 0; j < NJ; ++j) acc[mt][j][0] = acc[mt][j][1] = acc[mt][j][2] = acc[mt][j][3] = 0.f;
         // ldmatrix addressing: lane i feeds row (i % 8) of 8x8 matrix i / 8 --
@@ -740,11 +741,11 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
         const uint32_t bbase = smem_u32(Bm) + (uint32_t)((lr * kBmStride + (lm & 1) * 4) * 4);
 #pragma unroll
         for (int kk = 0; kk < kD / 8; ++kk) {
-            uint32_t ahi[2][4], alo[2][4];
+            uint32_t ahi[MTW][4], alo[MTW][4];
 #pragma unroll
-            for (int mt = 0; mt < 2; ++mt) {
+            for (int mt = 0; mt < MTW; ++mt) {
                 uint32_t x[4];
-                ldsm_x4(x, abase + (kk >> 2) * (TPC * 4096) + mt * 2048 + aoff[kk & 3]);
+                ldsm_x4(x, abase + (kk >> 2) * (TPC * 4096) + (half * MTW + mt) * 2048 + aoff[kk & 3]);
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     const uint32_t hi = x[q] & 0xFFFFE000u;
@@ -755,9 +756,16 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
 #pragma unroll
             for (int j = 0; j < NJ; ++j) {
                 uint32_t b[2];
-                ldsm_x2(b, bbase + (uint32_t)((j * 8 * kBmStride + kk * 8) * 4));
+                if constexpr (isz == 2) {   // bf16 row (vector j*8+g): exact in tf32, widened in registers
+                    const unsigned short *br = reinterpret_cast<const unsigned short *>(smem + L.Ap) +
+                                               (j * 8 + (lane >> 2)) * kKp + kk * 8 + (lane & 3);
+                    b[0] = (uint32_t)br[0] << 16;
+                    b[1] = (uint32_t)br[4] << 16;
+                } else {
+                    ldsm_x2(b, bbase + (uint32_t)((j * 8 * kBmStride + kk * 8) * 4));
+                }
 #pragma unroll
-                for (int mt = 0; mt < 2; ++mt) {
+                for (int mt = 0; mt < MTW; ++mt) {
                     mma_tf32_16x8x8(acc[mt][j], ahi[mt], b[0], b[1]);
                     mma_tf32_16x8x8(acc[mt][j], alo[mt], b[0], b[1]);
                 }
@@ -765,7 +773,7 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
                     uint32_t bl[2];
                     ldsm_x2(bl, bbase + (uint32_t)(((NB + j * 8) * kBmStride + kk * 8) * 4));
 #pragma unroll
-                    for (int mt = 0; mt < 2; ++mt) mma_tf32_16x8x8(acc[mt][j], ahi[mt], bl[0], bl[1]);
+                    for (int mt = 0; mt < MTW; ++mt) mma_tf32_16x8x8(acc[mt][j], ahi[mt], bl[0], bl[1]);
                 }
             }
         }
@@ -775,8 +783,8 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
             const int t = 4 * j + t4;
             if (t < n_new) {
 #pragma unroll
-                for (int mt = 0; mt < 2; ++mt) {
-                    const int row = mt * 16 + g;
+                for (int mt = 0; mt < MTW; ++mt) {
+                    const int row = (half * MTW + mt) * 16 + g;
                     av[(wt * NT + t) * 32 + row] = acc[mt][j][0];
                     bv[(wt * NT + t) * 32 + row] = acc[mt][j][1];
                     av[(wt * NT + t) * 32 + row + 8] = acc[mt][j][2];
@@ -1102,7 +1110,7 @@ cudaError_t launch_state(const ChunkArgs &a, cudaStream_t s) {
     // 2 or more new tokens (verify, prefill chunks): the state mat-vecs on the
     // warp-level tensor cores in the 2-warp CTA (mma.sync tf32, no TMEM);
     // the CUDA-core pass is the fallback without a tensor map
-    if (a.n_new >= 2 && a.tmap) return launch_nt<InT, UT, kChunkTPC, 1, true, 0, false, true>(a, s);
+    if (a.n_new >= 2 && a.tmap) return launch_nt<InT, UT, kChunkTPC, kMmaWPT, true, 0, false, true>(a, s);
     return launch_nt<InT, UT, kChunkTPC, 1, true>(a, s);
 }
 

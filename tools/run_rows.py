@@ -1,6 +1,7 @@
 """Profiling driver for the config-3 / config-4 kernels:
   python tools/run_rows.py verify   -- batch 256, 4 drafts: verify + commit, x reps
   python tools/run_rows.py direct   -- batch 1024, context 64: direct decode steps
+  python tools/run_rows.py rverify  -- batch 256, 4 drafts: recurrent verify + copy commit
 (for `ncu -k regex:chunk_cta` / `regex:fold`)."""
 import os
 import sys
@@ -25,6 +26,18 @@ if what == "verify":
     for _ in range(reps):
         buf.verify_drafts(0, x["q"], x["k"], x["v"], x["alpha"], x["beta"], o)
         buf.commit_accepted(0, na)
+elif what == "rverify":
+    B, N = 256, 4
+    buf = L.LaBuf(L.make_config(B, Hk, Hv, chunk=16, max_drafts=N), device="cuda")
+    buf.reset(zero_state=False)
+    buf.state.copy_(sd.state0(1, B, Hv))
+    x = sd.tokens(5, B, N, Hk, Hv)
+    o = torch.empty(B, N, Hv, 128, device="cuda")
+    temp = torch.empty(B, N, Hv, 128, 128, device="cuda")
+    na = sd.n_accepted(6, B, N)
+    for _ in range(reps):
+        buf.recurrent_verify(0, x["q"], x["k"], x["v"], x["alpha"], x["beta"], temp, o)
+        buf.recurrent_commit(0, na, temp)
 else:
     B, L0 = 1024, 64
     buf = L.LaBuf(L.make_config(B, Hk, Hv, chunk=16, short_cap=128, u_dtype="f16"), device="cuda")
