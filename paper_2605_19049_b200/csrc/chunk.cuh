@@ -43,7 +43,7 @@
 namespace labuf {
 
 constexpr int kChunkTPC = 2;        // d_v tiles (warps) per CTA for the state kinds
-constexpr int kMmaWPT = 1;          // warps per d_v tile for the multi-token (warp-MMA) kinds (2: measured
+constexpr int kMmaWPT = 1;  // (must be 1: the substitution lane of a row holds its MMA results)          // warps per d_v tile for the multi-token (warp-MMA) kinds (2: measured
                                     // slower for verify: N = 4 163 -> 176 us, N = 8 265 -> 293 us)
 constexpr int kDirectTPC = 4;       // ... and for direct slots (the key rows dominate)
 
@@ -75,31 +75,37 @@ __host__ __device__ inline CtaLayout cta_layout(int TPC, int nt, bool has_state,
     const int J = jcap + nt;
     uint32_t o = 0;
     // (tc / mma: 1 KiB of slack so the 128-byte-swizzled state tile starts 1024-aligned)
-    L.S = o;  o = al128(o + (has_state ? (uint32_t)(TPC * 32 * kD * 4) + (tc || mma ? 1024u : 0u) : 0u));
+    // (tc: 1 KiB of slack for the 1024-aligned swizzled tile; the MMA kinds rely
+    // on the dynamic shared memory base being 1024-aligned -- measured on B200,
+    // tools/probe_smem_align.cu -- and trap otherwise)
+    L.S = o;  o = al128(o + (has_state ? (uint32_t)(TPC * 32 * kD * 4) + (tc ? 1024u : 0u) : 0u));
     L.U = o;  o = al128(o + (uint32_t)(TPC * 32 * jcap * usz));
     L.K = o;  o = al128(o + (uint32_t)(jcap * kD * isz));
     L.Gs = o; o = al128(o + (uint32_t)(((jcap + 3) & ~3) * 4));
-    L.q = o;  o = al128(o + (uint32_t)(nt * kD * isz));
-    L.k = o;  o = al128(o + (uint32_t)(nt * kD * isz));
+    // (key-rows MMA kinds: q_t, k_t land straight in the padded rows Ap)
+    const bool krm_ = mma && isz == 2;
+    L.q = o;  o = al128(o + (krm_ ? 0u : (uint32_t)(nt * kD * isz)));
+    L.k = o;  o = al128(o + (krm_ ? 0u : (uint32_t)(nt * kD * isz)));
     L.v = o;  o = al128(o + (uint32_t)(nt * TPC * 32 * isz));
-    L.kq32 = o; o = al128(o + (nt > 1 && isz == 2 ? (uint32_t)(nt * 2 * kD * 4) : 0u));   // fp32 k_t, q_t
+    L.kq32 = o; o = al128(o + (nt > 1 && isz == 2 && !mma ? (uint32_t)(nt * 2 * kD * 4) : 0u));   // fp32 k_t, q_t
     // Ck / Cq are record-major [i][t] (rows of ntp(nt) floats): the records sum
     // reads all tokens' coefficients of a record with 16-byte loads
     L.Ck = o; o = al128(o + (uint32_t)(ntp(nt) * J * 4));
     L.Cq = o; o = al128(o + (uint32_t)(ntp(nt) * J * 4));
-    L.av = o; o = al128(o + (uint32_t)(has_state ? TPC * nt * 32 * 4 : 0));
-    L.bv = o; o = al128(o + (uint32_t)(has_state ? TPC * nt * 32 * 4 : 0));
+    // (the MMA kinds keep S0 k_t, S0 q_t in registers and shuffle them to the rows)
+    L.av = o; o = al128(o + (uint32_t)(has_state && !mma ? TPC * nt * 32 * 4 : 0));
+    L.bv = o; o = al128(o + (uint32_t)(has_state && !mma ? TPC * nt * 32 * 4 : 0));
     L.Gn = o; o = al128(o + (uint32_t)(nt * 4));
     L.Bn = o; o = al128(o + (uint32_t)(nt * 4));
     L.Y = o;  o = al128(o + (tc ? (uint32_t)(tc_nmma(nt) * kD * 4 * (isz == 4 ? 2 : 1)) : 0u));
-    L.Kf = o; o = al128(o + (fold ? (uint32_t)(TPC * 32 * kAuS * 4) : 0u));   // fused fold: A = U~ rows
+    L.Kf = o;   // (unused: the fused fold builds its operand in registers)
     // (fp32 tokens only: bf16 tokens feed the state pass from the bf16 rows Ap)
     L.Bm = o; o = al128(o + (mma && isz == 4 ? (uint32_t)(mma_nrows(nt) * kBmStride * 4 * 2) : 0u));
     // key rows on the tensor cores (bf16 inputs): the 2 nt vectors and the J
     // keys as bf16 rows padded to 272 B (conflict-free ldmatrix)
     const bool krm = mma && isz == 2;
-    L.Ap = o; o = al128(o + (krm ? (uint32_t)(((2 * nt + 15) / 16 * 16) * kKp * 2) : 0u));
-    L.Kp = o; o = al128(o + (krm ? (uint32_t)(((J + 7) / 8 * 8) * kKp * 2) : 0u));
+    L.Ap = o; o = al128(o + (krm ? (uint32_t)(2 * nt * kKp * 2) : 0u));   // (fragment rows past 2 nt clamp)
+    L.Kp = o; o = al128(o + (krm ? (uint32_t)(jcap * kKp * 2) : 0u));   // the buffered records' keys
     L.bar = o; o += 64;
     L.bytes = al128(o);
     return L;
@@ -256,13 +262,20 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
     uint64_t *tokb = MMA ? full + 5 : full;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + L.bar + 32);
     unsigned char *S_base = smem + L.S;
-    if constexpr (TC || MMA) S_base += (1024u - (smem_u32(S_base) & 1023u)) & 1023u;
+    if constexpr (TC) S_base += (1024u - (smem_u32(S_base) & 1023u)) & 1023u;
+    if constexpr (MMA) {
+        if (smem_u32(S_base) & 1023u) __trap();   // the swizzled TMA tile needs 1024-byte alignment
+    }
     const float *S_s = reinterpret_cast<const float *>(S_base);
     const UT *U_s = reinterpret_cast<const UT *>(smem + L.U);
     const InT *K_s = reinterpret_cast<const InT *>(smem + L.K);
     const float *G_s = reinterpret_cast<const float *>(smem + L.Gs);
-    const InT *q_s = reinterpret_cast<const InT *>(smem + L.q);
-    const InT *k_s = reinterpret_cast<const InT *>(smem + L.k);
+    // new tokens' q_t / k_t rows: token t at q_s + t * TS (key-rows MMA kinds: rows
+    // 2t + 1 / 2t of the padded bf16 operand Ap)
+    constexpr bool KRM = MMA && isz == 2;
+    constexpr int TS = KRM ? 2 * kKp : kD;
+    const InT *q_s = KRM ? reinterpret_cast<const InT *>(smem + L.Ap) + kKp : reinterpret_cast<const InT *>(smem + L.q);
+    const InT *k_s = KRM ? reinterpret_cast<const InT *>(smem + L.Ap) : reinterpret_cast<const InT *>(smem + L.k);
     const InT *v_s = reinterpret_cast<const InT *>(smem + L.v);
     float *Ck = reinterpret_cast<float *>(smem + L.Ck);
     float *Cq = reinterpret_cast<float *>(smem + L.Cq);
@@ -396,9 +409,9 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
         for (int c = lane; c < 3 * n_new; c += 32) {
             const int t = c % n_new, kind = c / n_new;
             if (kind == 0)
-                bulk_g2s(smem + L.q + (size_t)t * kD * isz, qin + (tok_of(t) * Hk + hk) * kD, kD * isz, tokb);
+                bulk_g2s(const_cast<InT *>(q_s) + (size_t)t * TS, qin + (tok_of(t) * Hk + hk) * kD, kD * isz, tokb);
             else if (kind == 1)
-                bulk_g2s(smem + L.k + (size_t)t * kD * isz, kin + (tok_of(t) * Hk + hk) * kD, kD * isz, tokb);
+                bulk_g2s(const_cast<InT *>(k_s) + (size_t)t * TS, kin + (tok_of(t) * Hk + hk) * kD, kD * isz, tokb);
             else
                 bulk_g2s(smem + L.v + (size_t)t * TPC * 32 * isz, vin + (tok_of(t) * Hv + h) * kD + tile0 * 32,
                          TPC * 32 * isz, tokb);
@@ -430,16 +443,16 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
     constexpr bool KQB = MMA && isz == 2;
     float *kq32 = reinterpret_cast<float *>(smem + L.kq32);
     float *Bm = reinterpret_cast<float *>(smem + L.Bm);
-    if constexpr (MMA) {
-        // B operand of the warp-MMA pass: row n = k_t (n = 2t) / q_t (n = 2t + 1),
-        // zero rows past 2 n_new; fp32 tokens split hi (top 19 bits) + lo
+    if constexpr (MMA && isz == 4) {
+        // B operand of the warp-MMA pass for fp32 tokens: row n = k_t (n = 2t) /
+        // q_t (n = 2t + 1), zero rows past 2 n_new, split hi (top 19 bits) + lo
+        // (bf16 tokens: the padded bf16 rows Ap serve both MMA passes as they land)
         constexpr int NB = mma_nrows(NT);
-        // 8 consecutive elements per step: one 16-byte bf16 load (or two fp32)
         for (int e = tid; e < NB * (kD / 8); e += NTHR) {
             const int n = e >> 4, c = (e & 15) * 8, t = n >> 1;
             float x[8];
             if (t < n_new) {
-                const InT *src = ((n & 1) ? q_s : k_s) + t * kD + c;
+                const InT *src = ((n & 1) ? q_s : k_s) + t * TS + c;
                 const float4 lo4 = load4(src), hi4 = load4(src + 4);
                 x[0] = lo4.x; x[1] = lo4.y; x[2] = lo4.z; x[3] = lo4.w;
                 x[4] = hi4.x; x[5] = hi4.y; x[6] = hi4.z; x[7] = hi4.w;
@@ -447,23 +460,15 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
 #pragma unroll
                 for (int i = 0; i < 8; ++i) x[i] = 0.f;
             }
-            float4 *dst = reinterpret_cast<float4 *>(Bm + n * kBmStride + c);
-            if constexpr (isz == 2) {   // bf16 tokens: the padded bf16 rows serve both MMA passes
-                if (n < 2 * NT) {
-                    const InT *src = ((n & 1) ? q_s : k_s) + t * kD + c;
-                    *reinterpret_cast<uint4 *>(reinterpret_cast<InT *>(smem + L.Ap) + n * kKp + c) =
-                        t < n_new ? *reinterpret_cast<const uint4 *>(src) : make_uint4(0u, 0u, 0u, 0u);
-                }
-            } else {
-                float hi[8], lo[8];
+            float hi[8], lo[8];
 #pragma unroll
-                for (int i = 0; i < 8; ++i) { hi[i] = trunc_tf32(x[i]); lo[i] = x[i] - hi[i]; }
-                dst[0] = make_float4(hi[0], hi[1], hi[2], hi[3]);
-                dst[1] = make_float4(hi[4], hi[5], hi[6], hi[7]);
-                float4 *dl = reinterpret_cast<float4 *>(Bm + (NB + n) * kBmStride + c);
-                dl[0] = make_float4(lo[0], lo[1], lo[2], lo[3]);
-                dl[1] = make_float4(lo[4], lo[5], lo[6], lo[7]);
-            }
+            for (int i = 0; i < 8; ++i) { hi[i] = trunc_tf32(x[i]); lo[i] = x[i] - hi[i]; }
+            float4 *dst = reinterpret_cast<float4 *>(Bm + n * kBmStride + c);
+            dst[0] = make_float4(hi[0], hi[1], hi[2], hi[3]);
+            dst[1] = make_float4(hi[4], hi[5], hi[6], hi[7]);
+            float4 *dl = reinterpret_cast<float4 *>(Bm + (NB + n) * kBmStride + c);
+            dl[0] = make_float4(lo[0], lo[1], lo[2], lo[3]);
+            dl[1] = make_float4(lo[4], lo[5], lo[6], lo[7]);
         }
     }
     if constexpr (KQ32) {
@@ -473,7 +478,7 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
             kq32[(t * 2 + 1) * kD + c] = to_f(q_s[e]);
         }
     }
-    if constexpr (KQ32 || MMA) __syncthreads();
+    if constexpr (KQ32 || (MMA && isz == 4)) __syncthreads();
     uint32_t tmem = 0;
     float *Yh = reinterpret_cast<float *>(smem + L.Y);
     float *Yl = Yh + NMMA * kD;
@@ -514,6 +519,8 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
         }
     }
     int j0 = 0, J = 0;
+    // MMA kinds: the state pass accumulators (S0 k_t, S0 q_t per row) live on in registers
+    float macc[MMA ? 2 / WPT : 1][MMA ? mma_nrows(NT) / 8 : 1][4];
     float gn_l = 0.f;
     // ---- 2. rows with 4-lane teams, 8 rows per warp step:
     //      state rows of the warp's tile: a = S0 k_t, b = S0 q_t;
@@ -645,16 +652,15 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
             // accumulate); keys = the j0 records then the new tokens' keys
             constexpr int NW = TPC * WPT, MT2 = (2 * NT + 15) / 16;
             InT *Kp = reinterpret_cast<InT *>(smem + L.Kp);
-            for (int e = tid; e < KS * 8 * (kD / 8); e += NTHR) {
+            for (int e = tid; e < j0 * (kD / 8); e += NTHR) {   // the records' keys, padded rows
                 const int i = e >> 4, c = (e & 15) * 8;
-                uint4 x = make_uint4(0u, 0u, 0u, 0u);
-                if (i < J) x = *reinterpret_cast<const uint4 *>((i < j0 ? K_s + (size_t)i * kD : k_s + (size_t)(i - j0) * kD) + c);
-                *reinterpret_cast<uint4 *>(Kp + i * kKp + c) = x;
+                *reinterpret_cast<uint4 *>(Kp + i * kKp + c) = *reinterpret_cast<const uint4 *>(K_s + (size_t)i * kD + c);
             }
-            __syncthreads();   // Kp, Gn_s (and Ap, written with Bm) visible
+            __syncthreads();   // Kp, Gn_s (and the token rows Ap) visible
             const int g = lane >> 2, t4 = lane & 3, lr = lane & 7, lm = lane >> 3;
-            const uint32_t ap = smem_u32(smem + L.Ap) + (uint32_t)(((lr + (lm & 1) * 8) * kKp + (lm >> 1) * 8) * 2);
-            const uint32_t kp = smem_u32(Kp) + (uint32_t)((lr * kKp + (lm & 1) * 8) * 2);
+            const uint32_t ap0 = smem_u32(smem + L.Ap) + (uint32_t)((lm >> 1) * 8 * 2);
+            const uint32_t apk = smem_u32(smem + L.Ap) + (uint32_t)((lm & 1) * 8 * 2);
+            const uint32_t kpb = smem_u32(Kp) + (uint32_t)((lm & 1) * 8 * 2);
             for (int nt = warp; nt < KS; nt += NW) {
 #pragma unroll
                 for (int mt = 0; mt < MT2; ++mt) {
@@ -662,8 +668,15 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
 #pragma unroll
                     for (int kk = 0; kk < kD / 16; ++kk) {
                         uint32_t av4[4], bv2[2];
-                        ldsm_x4(av4, ap + (uint32_t)((mt * 16 * kKp + kk * 16) * 2));
-                        ldsm_x2(bv2, kp + (uint32_t)((nt * 8 * kKp + kk * 16) * 2));
+                        // (rows past 2 NT repeat the last vector: their outputs are dropped)
+                        const int arow = min(mt * 16 + lr + (lm & 1) * 8, 2 * NT - 1);
+                        ldsm_x4(av4, ap0 + (uint32_t)((arow * kKp + kk * 16) * 2));
+                        // key row i: a buffered record (Kp) or new token i - j0 (row 2 (i - j0) of Ap;
+                        // rows past J repeat a valid row, their outputs are dropped)
+                        const int ki = nt * 8 + lr;
+                        const uint32_t brow = ki < j0 ? kpb + (uint32_t)(ki * kKp * 2)
+                                                      : apk + (uint32_t)(2 * min(ki - j0, n_new - 1) * kKp * 2);
+                        ldsm_x2(bv2, brow + (uint32_t)(kk * 16 * 2));
                         mma_bf16_16x8x16(acc, av4, bv2[0], bv2[1]);
                     }
 #pragma unroll
@@ -714,6 +727,7 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
     }
     if constexpr (MMA) {
         mbar_wait(full, 0);   // the state tile (TMA, swizzled)
+        float (&acc)[2 / WPT][mma_nrows(NT) / 8][4] = macc;
         // warp-level tensor cores (mma.sync m16n8k8 tf32, fp32 accumulate):
         // D[32 rows x 2NT] = S0 tile [32 x 128] . [k_t | q_t] [128 x 2NT];
         // A fragments straight from the 128-byte-swizzled tile (conflict-
@@ -721,8 +735,6 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
         // bf16 tokens (exact in tf32), 3 for fp32 tokens (+ hi . B_lo)
         constexpr int NB = mma_nrows(NT), NJ = NB / 8;
         constexpr int MTW = 2 / WPT;                 // m16 tiles of the 32-row tile per warp
-        const int g = lane >> 2, t4 = lane & 3;
-        float acc[MTW][NJ][4];
 #pragma unroll
         for (int mt = 0; mt < MTW; ++mt)
 #pragma unroll
@@ -758,7 +770,7 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
                 uint32_t b[2];
                 if constexpr (isz == 2) {   // bf16 row (vector j*8+g): exact in tf32, widened in registers
                     const unsigned short *br = reinterpret_cast<const unsigned short *>(smem + L.Ap) +
-                                               (j * 8 + (lane >> 2)) * kKp + kk * 8 + (lane & 3);
+                                               min(j * 8 + (lane >> 2), 2 * NT - 1) * kKp + kk * 8 + (lane & 3);
                     b[0] = (uint32_t)br[0] << 16;
                     b[1] = (uint32_t)br[4] << 16;
                 } else {
@@ -777,21 +789,8 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
                 }
             }
         }
-        // D[row][2 t + {0, 1}] = (S0 k_t, S0 q_t) of token t = 4 j + t4
-#pragma unroll
-        for (int j = 0; j < NJ; ++j) {
-            const int t = 4 * j + t4;
-            if (t < n_new) {
-#pragma unroll
-                for (int mt = 0; mt < MTW; ++mt) {
-                    const int row = (half * MTW + mt) * 16 + g;
-                    av[(wt * NT + t) * 32 + row] = acc[mt][j][0];
-                    bv[(wt * NT + t) * 32 + row] = acc[mt][j][1];
-                    av[(wt * NT + t) * 32 + row + 8] = acc[mt][j][2];
-                    bv[(wt * NT + t) * 32 + row + 8] = acc[mt][j][3];
-                }
-            }
-        }
+        // D[row][2 t + {0, 1}] = (S0 k_t, S0 q_t) of token t = 4 j + t4: stays in
+        // registers; the substitution shuffles each row's values to its lane
     }
     if constexpr (TC) {
         // pass 2 on the exact remainder S0 - trunc(S0), written in place once
@@ -828,7 +827,7 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
     }
     if (dm.validate) {
         for (int e = tid; e < n_new * kD; e += NTHR) {
-            const float kk = to_f(k_s[e]), qq = to_f(q_s[e]);
+            const float kk = to_f(k_s[(e / kD) * TS + e % kD]), qq = to_f(q_s[(e / kD) * TS + e % kD]);
             if (!(isfinite(kk) && isfinite(qq))) bad |= 0x4u;
         }
     }
@@ -918,7 +917,24 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
                 const float bt = Bn_s[t];
                 const float eG = expf(Gn_s[t]);
                 float u, o;
-                if (HAS_STATE) {
+                if constexpr (MMA) {
+                    // (S0 k_t, S0 q_t) of this row from the fragment holder: lane
+                    // 4 (row % 8) + t % 4 holds rows g, g + 8 of each m-tile
+                    static_assert(!MMA || WPT == 1, "row = lane");
+                    const int src = 4 * (row & 7) + (t & 3), j = t >> 2;
+                    const float a00 = __shfl_sync(0xffffffffu, macc[0][j][0], src);
+                    const float a08 = __shfl_sync(0xffffffffu, macc[0][j][2], src);
+                    const float a10 = __shfl_sync(0xffffffffu, macc[MMA ? 1 : 0][j][0], src);
+                    const float a18 = __shfl_sync(0xffffffffu, macc[MMA ? 1 : 0][j][2], src);
+                    const float b00 = __shfl_sync(0xffffffffu, macc[0][j][1], src);
+                    const float b08 = __shfl_sync(0xffffffffu, macc[0][j][3], src);
+                    const float b10 = __shfl_sync(0xffffffffu, macc[MMA ? 1 : 0][j][1], src);
+                    const float b18 = __shfl_sync(0xffffffffu, macc[MMA ? 1 : 0][j][3], src);
+                    const float ar = row < 16 ? (row & 8 ? a08 : a00) : (row & 8 ? a18 : a10);
+                    const float br = row < 16 ? (row & 8 ? b08 : b00) : (row & 8 ? b18 : b10);
+                    u = bt * (vt - fmaf(eG, ar, acc_k));
+                    o = fmaf(eG, br, acc_q);
+                } else if (HAS_STATE) {
                     u = bt * (vt - fmaf(eG, av[(wt * NT + t) * 32 + row], acc_k));
                     o = fmaf(eG, bv[(wt * NT + t) * 32 + row], acc_q);
                 } else {
@@ -949,16 +965,33 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
                 // (split TF32: U~ hi + lo; bf16 keys exact, fp32 keys hi + lo), J padded to 8
                 const float gt = Gn_s[0];
                 const float eG = expf(gt);
-                float *Au = reinterpret_cast<float *>(smem + L.Kf) + (size_t)wt * 32 * kAuS;
-#pragma unroll
-                for (int i = 0; i < kFusedFoldMaxC; ++i)
-                    Au[row * kAuS + i] = i < j0 ? expf(gt - G_s[i]) * to_f(ut[(size_t)i * kUSub]) : (i == j0 ? un[0] : 0.f);
-                __syncwarp();
-                const int g = lane >> 2, t4 = lane & 3, lr = lane & 7, lm = lane >> 3;
+                const int g = lane >> 2, t4 = lane & 3;
                 const int KS = (J + 7) / 8;
                 auto key = [&](int i, int c) -> float { return i < J ? to_f(i < j0 ? K_s[i * kD + c] : k_s[c]) : 0.f; };
                 float *Sw = const_cast<float *>(S_s) + (size_t)wt * 32 * kD;
-                const uint32_t au = smem_u32(Au) + (uint32_t)(((lr + (lm & 1) * 8) * kAuS + (lm >> 1) * 4) * 4);
+                // A = U~ fragments in registers, once: U~[row][i] = e^{G_t-G_i} u_i[row] from the
+                // staged records (i < j0) and the new token's u_t (i = j0, lane `row` holds it)
+                const UT *uw = U_s + (size_t)wt * j0 * kUSub;
+                uint32_t fhi[kFusedFoldMaxC / 8][2][4], flo[kFusedFoldMaxC / 8][2][4];
+#pragma unroll
+                for (int ks = 0; ks < kFusedFoldMaxC / 8; ++ks) {
+                    if (ks < KS) {
+#pragma unroll
+                        for (int mt = 0; mt < 2; ++mt) {
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) {
+                                const int rr = mt * 16 + g + (q & 1) * 8, i = ks * 8 + t4 + (q >> 1) * 4;
+                                const float un_r = __shfl_sync(0xffffffffu, un[0], rr);
+                                float x = 0.f;
+                                if (i < j0) x = expf(gt - G_s[i]) * to_f(uw[(size_t)i * kUSub + rr]);
+                                else if (i == j0) x = un_r;
+                                const uint32_t hi = __float_as_uint(x) & 0xFFFFE000u;
+                                fhi[ks][mt][q] = hi;
+                                flo[ks][mt][q] = __float_as_uint(x - __uint_as_float(hi));
+                            }
+                        }
+                    }
+                }
 #pragma unroll 1
                 for (int ng = 0; ng < kD / 32; ++ng) {
                     float acc[2][4][4];
@@ -966,20 +999,11 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
                     for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
                         for (int nt = 0; nt < 4; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = acc[mt][nt][2] = acc[mt][nt][3] = 0.f;
-#pragma unroll 1
-                    for (int ks = 0; ks < KS; ++ks) {
-                        uint32_t ahi[2][4], alo[2][4];
 #pragma unroll
-                        for (int mt = 0; mt < 2; ++mt) {
-                            uint32_t x[4];
-                            ldsm_x4(x, au + (uint32_t)((mt * 16 * kAuS + ks * 8) * 4));
-#pragma unroll
-                            for (int q = 0; q < 4; ++q) {
-                                const uint32_t hi = x[q] & 0xFFFFE000u;
-                                ahi[mt][q] = hi;
-                                alo[mt][q] = __float_as_uint(__uint_as_float(x[q]) - __uint_as_float(hi));
-                            }
-                        }
+                    for (int ks = 0; ks < kFusedFoldMaxC / 8; ++ks) {
+                        if (ks >= KS) break;
+                        const uint32_t (&ahi)[2][4] = fhi[ks];
+                        const uint32_t (&alo)[2][4] = flo[ks];
 #pragma unroll
                         for (int nt = 0; nt < 4; ++nt) {
                             const int c = ng * 32 + nt * 8 + g;
@@ -1032,7 +1056,8 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
             if (h % dm.g == 0) {
                 for (int idx = tid; idx < n_new * kD; idx += NTHR) {
                     const int2 rp = recpos(idx / kD);
-                    static_cast<InT *>(a.p.K)[(((size_t)rp.x * Hk + hk) * dm.bt + rp.y) * kD + idx % kD] = k_s[idx];
+                    static_cast<InT *>(a.p.K)[(((size_t)rp.x * Hk + hk) * dm.bt + rp.y) * kD + idx % kD] =
+                        k_s[(idx / kD) * TS + idx % kD];
                 }
             }
             if (tid < n_new) {
@@ -1042,7 +1067,7 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
         } else {
             if (h % dm.g == 0) {
                 InT *Kdst = static_cast<InT *>(a.p.K) + (((size_t)r * Hk + hk) * T + j0) * kD;
-                for (int idx = tid; idx < n_new * kD; idx += NTHR) Kdst[idx] = k_s[idx];
+                for (int idx = tid; idx < n_new * kD; idx += NTHR) Kdst[idx] = k_s[(idx / kD) * TS + idx % kD];
             }
             if (tid < n_new) a.p.G[((size_t)r * Hv + h) * T + j0 + tid] = Gn_s[tid];
         }

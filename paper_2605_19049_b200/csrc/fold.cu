@@ -91,7 +91,7 @@ __global__ void __launch_bounds__(kFoldThreads, RAW ? 4 : (kFoldNJ == 128 ? 2 : 
     uint64_t *bar_ld = reinterpret_cast<uint64_t *>(smem + L.bar);
     uint64_t *bar_mma = bar_ld + 1;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bar_ld + 2);
-    int *meta = reinterpret_cast<int *>(bar_ld + 3);      // n, zero_s0
+    int *meta = reinterpret_cast<int *>(bar_ld + 3);      // n, zero_s0, branch occ / offset, G_last
     const size_t sb = PG && a.p.sidx ? (size_t)__ldcg(a.p.sidx + r) : (size_t)r;
     float *state_tile = a.p.state + ((sb * Hv + h) * kD + (size_t)jh * kFoldNJ) * kD;
     // where S_new goes: the slot's own state, or (FK_FORK) the destination slot's
@@ -201,6 +201,13 @@ __global__ void __launch_bounds__(kFoldThreads, RAW ? 4 : (kFoldNJ == 128 ? 2 : 
         }
         meta[0] = n;
         meta[1] = zero_s0;
+        // the last folded record's log decay, read here with the counters (off
+        // the post-barrier critical path); branch commits remap past occ
+        if (n > 0) {
+            const int last = (a.kind == FK_BRANCH && n - 1 >= occ) ? n - 1 + meta[3] : n - 1;
+            const int2 ba = PG ? rec_at(dm, a.p, r, last) : make_int2(r, last);
+            meta[4] = __float_as_int(a.p.G[((size_t)ba.x * Hv + h) * bt + ba.y]);
+        }
         if (!a.spec && n > 0 && !zero_s0) {
             mbar_arrive_expect_tx(bar_ld, kFoldNJ * kD * 4);
             bulk_g2s(S_s, state_tile, kFoldNJ * kD * 4, bar_ld);
@@ -364,7 +371,7 @@ __global__ void __launch_bounds__(kFoldThreads, RAW ? 4 : (kFoldNJ == 128 ? 2 : 
         __syncthreads();
         load_chunk(0, min(KC, n));
     }
-    const float g_last = a.p.G[rec(n - 1)];
+    const float g_last = __int_as_float(meta[4]);
     const uint32_t idesc = idesc_tf32(128, kFoldNJ);
     uint32_t mma_phase = 0;
 
