@@ -224,7 +224,8 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
     constexpr int RPW = 32 / WPT;                // d_v rows per warp
     constexpr int V = 2 * NT;                    // reduced values per row: (k_t, q_t) dots
     constexpr int NOUT = TeamOut<V>::N;
-    constexpr bool KQ_REG = NT == 1;             // k_t, q_t chunks held in registers
+    constexpr bool KQ_REG = NT == 1 && HAS_STATE; // k_t, q_t chunks held in registers (decode; the
+                                                 // direct kind reads them from shared memory: registers)
     constexpr int isz = (int)sizeof(InT), usz = (int)sizeof(UT);
     static_assert(NT <= 32, "decay scan runs inside one warp");
     static_assert(NTHR >= 64, "warp 0 requests the records, warp 1 the new tokens");
@@ -1098,7 +1099,11 @@ static cudaError_t launch_cfg(const ChunkArgs &a, cudaStream_t s) {
                   : chunk_cta_kernel<InT, UT, TPC, WPT, NT, HAS_STATE, MINB < 1 ? 1 : MINB, TC, FOLD, MMA, false>;
     cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.bytes);
     if (e != cudaSuccess) return e;
-    if (a.dry) return cudaSuccess;   // configuration check only (all-or-nothing pre-pass)
+    if (a.dry) return cudaSuccess;
+    // the whole L1 / shared carveout for shared memory: CTAs per SM are bounded
+    // by registers and shared memory only, never by the driver's default split
+    e = cudaFuncSetAttribute(kfn, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+    if (e != cudaSuccess) return e;   // configuration check only (all-or-nothing pre-pass)
     CUtensorMap tm;
     if (TC || MMA) tm = *static_cast<const CUtensorMap *>(a.tmap);
     else memset(&tm, 0, sizeof(tm));
@@ -1121,7 +1126,7 @@ template <typename InT, typename UT>
 cudaError_t launch_direct(const ChunkArgs &a, cudaStream_t s) {
     // direct: at most 128 registers so 4 CTAs (16 warps) share an SM (measured
     // 338 -> 281 us at config 4; 5 CTAs spill more and lose)
-    return launch_nt<InT, UT, kDirectTPC, 1, false, 4>(a, s);
+    return launch_nt<InT, UT, kDirectTPC, 1, false, 5>(a, s);
 }
 
 template <typename InT, typename UT>

@@ -476,6 +476,10 @@ static cudaError_t launch_fold_cfg(const FoldArgs &a, cudaStream_t s) {
     auto kfn = pg ? fold_kernel<InT, UT, FP32_IN, NJ, KCM, RAW, true> : fold_kernel<InT, UT, FP32_IN, NJ, KCM, RAW, false>;
     cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
     if (e != cudaSuccess) return e;
+    // the whole L1 / shared carveout for shared memory: CTAs per SM are bounded
+    // by registers and shared memory only, never by the driver's default split
+    e = cudaFuncSetAttribute(kfn, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+    if (e != cudaSuccess) return e;
     return launch_k(kfn, dim3(kD / NJ, a.dm.Hv, a.n), dim3(kFoldThreads), L.total, s, a.pdl != 0, a);
 }
 

@@ -279,7 +279,8 @@ class LaBuf:
         (la_decode_mixed).  slots: host int sequence (numpy / list); tensors
         q,k [n,Hk,d], v [n,Hv,d], alpha,beta [n,Hv], o [n,Hv,d] by batch row."""
         import numpy as np
-        sl = np.ascontiguousarray(np.asarray(slots, dtype=np.int32))
+        sl = slots if isinstance(slots, np.ndarray) and slots.dtype == np.int32 and slots.flags.c_contiguous \
+            else np.ascontiguousarray(np.asarray(slots, dtype=np.int32))
         n = int(sl.shape[0])
         self._tok(n, 1, q.unsqueeze(1), k.unsqueeze(1), v.unsqueeze(1), alpha.unsqueeze(1),
                   beta.unsqueeze(1), o.unsqueeze(1))

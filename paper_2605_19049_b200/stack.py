@@ -246,6 +246,9 @@ class MixedStack:
         are the layer's [n, ...] tensors by batch row."""
         s = self.spec
         if slots is None:
-            slots = range(s.n_long + s.n_short)
+            if getattr(self, "_all_slots", None) is None:
+                import numpy as np
+                self._all_slots = np.arange(s.n_long + s.n_short, dtype=np.int32)
+            slots = self._all_slots
         for b, x, o in zip(self.layers, inputs, outputs):
             b.decode_mixed(slots, x["q"], x["k"], x["v"], x["alpha"], x["beta"], o)
