@@ -865,6 +865,9 @@ def extra_rows(torch, L, cost, dev, stream, seed, K, W, peak, args):
             "recurrent": int(180e9 // (36 * (N3 + 1) * lb.st)),
             "buffered": int(180e9 // (36 * (lb.st + bufs[0].sizes.capacity * lb.rec))),
             "buffered_records_reserved_per_slot": bufs[0].sizes.capacity,
+            # the paper's 5x counts one state plus the N draft records
+            # (a paged pool with blocks of N records, la_buf_query-sized)
+            "buffered_drafts_only": int(180e9 // (36 * (lb.st + N3 * lb.rec))),
         },
     }
     del gv, gc, grv, grc, gm, temps, bufs, xs

@@ -70,7 +70,7 @@ __host__ __device__ constexpr int mma_nrows(int nt) { return (2 * nt + 7) / 8 * 
 __host__ __device__ constexpr int tc_nmma(int nt) { return (2 * nt + 15) / 16 * 16; }
 
 __host__ __device__ inline CtaLayout cta_layout(int TPC, int nt, bool has_state, int jcap, int isz, int usz,
-                                                bool tc = false, bool fold = false, bool mma = false) {
+                                                bool tc = false, bool fold = false, bool mma = false, int minb = 1) {
     CtaLayout L;
     const int J = jcap + nt;
     uint32_t o = 0;
@@ -87,7 +87,9 @@ __host__ __device__ inline CtaLayout cta_layout(int TPC, int nt, bool has_state,
     L.q = o;  o = al128(o + (krm_ ? 0u : (uint32_t)(nt * kD * isz)));
     L.k = o;  o = al128(o + (krm_ ? 0u : (uint32_t)(nt * kD * isz)));
     L.v = o;  o = al128(o + (uint32_t)(nt * TPC * 32 * isz));
-    L.kq32 = o; o = al128(o + (nt > 1 && isz == 2 && !mma ? (uint32_t)(nt * 2 * kD * 4) : 0u));   // fp32 k_t, q_t
+    // fp32 k_t, q_t: the kinds that do not keep them in registers (KQ_REG)
+    const bool kq_reg = nt == 1 && (has_state || minb < 5);
+    L.kq32 = o; o = al128(o + (!kq_reg && isz == 2 && !mma ? (uint32_t)(nt * 2 * kD * 4) : 0u));
     // Ck / Cq are record-major [i][t] (rows of ntp(nt) floats): the records sum
     // reads all tokens' coefficients of a record with 16-byte loads
     L.Ck = o; o = al128(o + (uint32_t)(ntp(nt) * J * 4));
@@ -224,8 +226,9 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
     constexpr int RPW = 32 / WPT;                // d_v rows per warp
     constexpr int V = 2 * NT;                    // reduced values per row: (k_t, q_t) dots
     constexpr int NOUT = TeamOut<V>::N;
-    constexpr bool KQ_REG = NT == 1 && HAS_STATE; // k_t, q_t chunks held in registers (decode; the
-                                                 // direct kind reads them from shared memory: registers)
+    // k_t, q_t chunks held in registers (decode, and direct at the 4-CTA budget;
+    // the 5-CTA direct instantiation reads them from shared memory: registers)
+    constexpr bool KQ_REG = NT == 1 && (HAS_STATE || MINB < 5);
     constexpr int isz = (int)sizeof(InT), usz = (int)sizeof(UT);
     static_assert(NT <= 32, "decay scan runs inside one warp");
     static_assert(NTHR >= 64, "warp 0 requests the records, warp 1 the new tokens");
@@ -253,7 +256,7 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
     constexpr int NTP = ntp(NT);                 // row stride of Ck/Cq ([record][token])
 
     extern __shared__ __align__(1024) unsigned char smem[];
-    const CtaLayout L = cta_layout(TPC, NT, HAS_STATE, a.j0_cap, isz, usz, TC, FOLD, MMA);
+    const CtaLayout L = cta_layout(TPC, NT, HAS_STATE, a.j0_cap, isz, usz, TC, FOLD, MMA, MINB);
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + L.bar);
     uint64_t *recs = full + 1;                  // second barrier: the buffered records
     int *j0_s = reinterpret_cast<int *>(smem + L.bar + 16);
@@ -1088,10 +1091,10 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
 template <typename InT, typename UT, int TPC, int WPT, int NT, bool HAS_STATE, int MBO = 0, bool TC = false,
           bool FOLD = false, bool MMA = false>
 static cudaError_t launch_cfg(const ChunkArgs &a, cudaStream_t s) {
-    const CtaLayout L = cta_layout(TPC, NT, HAS_STATE, a.j0_cap, sizeof(InT), sizeof(UT), TC, FOLD, MMA);
+    constexpr int MINB = MBO ? MBO : (NT <= 2 ? (HAS_STATE ? 12 / (TPC * WPT) : 2) : 1);
+    const CtaLayout L = cta_layout(TPC, NT, HAS_STATE, a.j0_cap, sizeof(InT), sizeof(UT), TC, FOLD, MMA, MINB < 1 ? 1 : MINB);
     if (L.bytes > 227 * 1024) return cudaErrorInvalidConfiguration;
     if (a.n > kMaxSlotsPerLaunch) return cudaErrorInvalidConfiguration;
-    constexpr int MINB = MBO ? MBO : (NT <= 2 ? (HAS_STATE ? 12 / (TPC * WPT) : 2) : 1);
     // pools / index lists: the PG instantiation (not for the TC or fused-fold kinds)
     const bool pg = a.slots || a.pos || a.p.btab || a.p.sidx;
     if (pg && (TC || FOLD)) return cudaErrorInvalidValue;
@@ -1126,7 +1129,11 @@ template <typename InT, typename UT>
 cudaError_t launch_direct(const ChunkArgs &a, cudaStream_t s) {
     // direct: at most 128 registers so 4 CTAs (16 warps) share an SM (measured
     // 338 -> 281 us at config 4; 5 CTAs spill more and lose)
-    return launch_nt<InT, UT, kDirectTPC, 1, false, 5>(a, s);
+    // (short contexts: 5 CTAs per SM at <= 102 registers, k_t / q_t from shared
+    //  memory -- measured faster up to ~64 records; longer ones keep the
+    //  4-CTA budget with k_t / q_t in registers, faster at 100+ records)
+    if (a.j0_cap + a.n_new <= 64) return launch_nt<InT, UT, kDirectTPC, 1, false, 5>(a, s);
+    return launch_nt<InT, UT, kDirectTPC, 1, false, 4>(a, s);
 }
 
 template <typename InT, typename UT>

@@ -143,12 +143,16 @@ cudaError_t launch_recurrent_commit(const RecArgs &a, cudaStream_t s, int64_t *l
 // state indices, work lists): small host decisions delivered in stream order
 // as kernel parameters (no host buffer outlives the call; graph-capturable).
 constexpr int kStageMax = 3000;
-struct StageArgs {
+constexpr int kStageSmall = 256;   // the usual per-step update fits a 2 KiB parameter block
+template <int CAP>
+struct StageArgsT {
     int *dst;
     int n;
-    int2 e[kStageMax];   // (index, value)
+    int2 e[CAP];   // (index, value)
 };
-cudaError_t launch_stage(const StageArgs &a, cudaStream_t s, int64_t *launches);
+using StageArgs = StageArgsT<kStageMax>;
+// n entries from e[] (n <= kStageMax); the smallest parameter block that holds them
+cudaError_t launch_stage(int *dst, const int2 *e, int n, int pdl, cudaStream_t s, int64_t *launches);
 cudaError_t launch_reset(const Dims &dm, const Ptrs &p, int first, int n, int mode, int zero_state,
                          cudaStream_t s, int64_t *launches);
 

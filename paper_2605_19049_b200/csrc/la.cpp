@@ -73,6 +73,10 @@ struct la_buf {
     std::vector<int32_t> free_blocks, free_states;
     int *meta_i = nullptr;                           // device meta as int32
     std::vector<int32_t> wl_dev;                     // what the device work lists hold (-1: unknown)
+    // la_decode_mixed scratch (reused across calls: no per-call allocation)
+    std::vector<int> mx_cw, mx_cwp, mx_dr, mx_drp, mx_fl, mx_cp;
+    std::vector<uint32_t> mx_seen;
+    uint32_t mx_stamp = 0;
     size_t i_sidx = 0, i_btab = 0, i_wl = 0;         // int32 offsets in meta
     int64_t launches = 0;
     int overlap = 0;                                 // la_set_overlap
@@ -423,11 +427,8 @@ void drop_state(la_buf *b, int r) {
 }
 cudaError_t run_stage(la_buf *b, Stage &st, cudaStream_t s) {
     for (size_t o = 0; o < st.e.size(); o += kStageMax) {
-        StageArgs a;
-        a.dst = b->meta_i;
-        a.n = (int)std::min(st.e.size() - o, (size_t)kStageMax);
-        memcpy(a.e, st.e.data() + o, a.n * sizeof(int2));
-        cudaError_t e = launch_stage(a, s, &b->launches);
+        const int n = (int)std::min(st.e.size() - o, (size_t)kStageMax);
+        cudaError_t e = launch_stage(b->meta_i, st.e.data() + o, n, 1, s, &b->launches);
         if (e != cudaSuccess) return e;
         note_launch(b, s, true);   // state indices / tables moved: no early state loads next
     }
@@ -995,16 +996,21 @@ la_status la_decode_mixed(la_buf *b, int32_t n, const int32_t *slots, const void
     // route every slot to its form (host mirror): chunkwise decode (+ eager
     // flush of a buffer it fills), KV-only decode, or compression at
     // len == short_cap followed by chunkwise decode
-    std::vector<int> cw, cw_pos, dr, dr_pos, fl, cp;
-    std::vector<char> seen(R, 0);
+    std::vector<int> &cw = b->mx_cw, &cw_pos = b->mx_cwp, &dr = b->mx_dr, &dr_pos = b->mx_drp, &fl = b->mx_fl,
+                     &cp = b->mx_cp;
+    cw.clear(); cw_pos.clear(); dr.clear(); dr_pos.clear(); fl.clear(); cp.clear();
+    if (b->mx_seen.size() != (size_t)R) b->mx_seen.assign(R, 0);
+    if (++b->mx_stamp == 0) { std::fill(b->mx_seen.begin(), b->mx_seen.end(), 0u); b->mx_stamp = 1; }
+    const uint32_t stamp = b->mx_stamp;
     std::vector<Grow> g;
+    if (b->paged) g.reserve(n);
     int j0_cw = 0, j0_dr = 0, cp_cap = 0;
     size_t need_states = 0;
     for (int i = 0; i < n; ++i) {
         const int r = slots[i];
         if (r < 0 || r >= R) return fail(LA_ERR_INVALID, "slots[%d] = %d outside [0, %d)", i, r, R);
-        if (seen[r]) return fail(LA_ERR_INVALID, "slot %d appears twice in the batch", r);
-        seen[r] = 1;
+        if (b->mx_seen[r] == stamp) return fail(LA_ERR_INVALID, "slot %d appears twice in the batch", r);
+        b->mx_seen[r] = stamp;
         if (b->pending[r]) return fail(LA_ERR_MODE, "slot %d has a pending verify (commit first)", r);
         if (b->mode[r] == LA_MODE_CHUNKWISE) {
             if (b->sidx[r] < 0) return fail(LA_ERR_MODE, "slot %d holds no state (reset it as CHUNKWISE)", r);

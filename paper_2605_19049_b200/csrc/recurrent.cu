@@ -7,6 +7,8 @@
 // Row j of the state evolves independently (north-star form):
 //   m_j = alpha (S0[j] . k);  u_j = beta (v_j - m_j);
 //   S[j] <- alpha S0[j] + u_j k;  o_j = S[j] . q = alpha (S0[j] . q) + u_j (k . q)
+#include <cstring>
+
 #include "device.cuh"
 #include "internal.h"
 
@@ -321,18 +323,29 @@ cudaError_t launch_commit_append(const Dims &dm, const Ptrs &p, int first, int n
 }
 
 // ------------------------------------------------------------------ stage
-__global__ void stage_kernel(const __grid_constant__ StageArgs a) {
+template <int CAP>
+__global__ void stage_kernel(const __grid_constant__ StageArgsT<CAP> a) {
     if (a.n > 0) pdl_wait();   // the previous grid may still read the entries being replaced
     pdl_trigger();
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += gridDim.x * blockDim.x)
         a.dst[a.e[i].x] = a.e[i].y;
 }
 
-cudaError_t launch_stage(const StageArgs &a, cudaStream_t s, int64_t *launches) {
-    if (a.n <= 0) return cudaSuccess;
-    cudaError_t e = launch_k(stage_kernel, dim3((a.n + 255) / 256), dim3(256), 0, s, true, a);
-    if (e == cudaSuccess) ++*launches;
-    return e;
+template <int CAP>
+static cudaError_t stage_cap(int *dst, const int2 *e, int n, cudaStream_t s) {
+    StageArgsT<CAP> a;
+    a.dst = dst;
+    a.n = n;
+    memcpy(a.e, e, n * sizeof(int2));
+    return launch_k(stage_kernel<CAP>, dim3((n + 255) / 256), dim3(256), 0, s, true, a);
+}
+
+cudaError_t launch_stage(int *dst, const int2 *e, int n, int /*pdl*/, cudaStream_t s, int64_t *launches) {
+    if (n <= 0) return cudaSuccess;
+    if (n > kStageMax) return cudaErrorInvalidValue;
+    cudaError_t err = n <= kStageSmall ? stage_cap<kStageSmall>(dst, e, n, s) : stage_cap<kStageMax>(dst, e, n, s);
+    if (err == cudaSuccess) ++*launches;
+    return err;
 }
 
 // ------------------------------------------------------------------ reset
