@@ -17,7 +17,7 @@ CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "liblabuf.so")
 
 CU_SOURCES = ["chunk.cu", "chunk_f32_direct.cu", "chunk_f32_state.cu", "chunk_bf16_direct.cu",
-              "chunk_bf16_state.cu", "chunk_bf16h_direct.cu", "chunk_bf16h_state.cu", "fold.cu", "recurrent.cu"]
+              "chunk_bf16_state.cu", "chunk_bf16h_direct.cu", "chunk_bf16h_state.cu", "fold.cu", "fold_ut.cu", "recurrent.cu"]
 CPP_SOURCES = ["la.cpp", "tp.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

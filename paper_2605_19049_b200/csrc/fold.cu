@@ -28,15 +28,12 @@
 namespace labuf {
 
 constexpr int kFoldKCMax = 16;   // tokens per MMA staging chunk (max)
-constexpr int kKs = 132;         // mode ii: fp32 key rows padded to 132 floats (conflict-free ldmatrix)
 constexpr int kFoldThreads = 128;
 
 struct FoldSmem {
-    uint32_t S, A, Alo, Bhi, Blo, bar, Ks, Gm, Us, Gs, Bs, total;
+    uint32_t S, A, Alo, Bhi, Blo, bar, total;
 };
-// raw_n > 0 (mode ii): room for the n raw keys (fp32), the n x n scaled Gram
-// matrix and the CTA's n x nj delta values recomputed by the UT transform
-__host__ __device__ inline FoldSmem fold_smem_layout(bool fp32_in, int nj, int kc, int raw_n = 0) {
+__host__ __device__ inline FoldSmem fold_smem_layout(bool fp32_in, int nj, int kc) {
     FoldSmem L;
     uint32_t o = 0;
     L.S = o;   o += (uint32_t)nj * kD * 4;                 // nj state rows
@@ -45,11 +42,6 @@ __host__ __device__ inline FoldSmem fold_smem_layout(bool fp32_in, int nj, int k
     L.Bhi = o; o += (uint32_t)nj * kc * 4;
     L.Blo = o; o += (uint32_t)nj * kc * 4;
     L.bar = o; o += 64;
-    L.Ks = o;  o += (uint32_t)((raw_n + 15) & ~15) * kKs * 4;   // rows past raw_n are zero
-    L.Gm = o;  o += (uint32_t)raw_n * raw_n * 4;
-    L.Us = o;  o += (uint32_t)raw_n * nj * 4;
-    L.Gs = o;  o += (uint32_t)raw_n * 4;
-    L.Bs = o;  o += (uint32_t)raw_n * 4;
     L.total = o;
     return L;
 }
@@ -61,18 +53,10 @@ __device__ __forceinline__ uint32_t kmaj_off(int row, int k, int kc) {
     return (uint32_t)((row >> 3) * (kc * 32) + (k >> 2) * 128 + (row & 7) * 16 + (k & 3) * 4);
 }
 
-// Mode ii (RAW, P:392-399 with reading Z4): the delta values are not read
-// from the buffer but recomputed from the raw records (k_i, v_i, beta_i, G_i)
-// and S0 by the UT transform, per d_v column j of the CTA's tile:
-//   W[i][j] = (S0 k_i)[j]                                     (CUDA cores)
-//   u_i[j]  = beta_i (v_i[j] - e^{G_i} W[i][j]
-//                     - sum_{l<i} e^{G_i-G_l} (k_i.k_l) u_l[j])  (forward substitution)
-// i.e. U = T Diag(beta) (V - Diag(e^G) W) with T = [I + strictLower(Diag(beta)
-// (Gamma (.) K K^T))]^{-1}, then the same tensor-core fold as mode i.
-template <typename InT, typename UT, bool FP32_IN, int kFoldNJ, int KCM, bool RAW, bool PG>
-__global__ void __launch_bounds__(kFoldThreads, RAW ? 4 : (kFoldNJ == 128 ? 2 : (kFoldNJ == 32 && KCM == 16 ? 8 : 4))) fold_kernel(const FoldArgs a) {
+// (Mode ii, the UT transform from the raw records, is fold_ut.cu.)
+template <typename InT, typename UT, bool FP32_IN, int kFoldNJ, int KCM, bool PG>
+__global__ void __launch_bounds__(kFoldThreads, kFoldNJ == 128 ? 2 : (kFoldNJ == 32 && KCM == 16 ? 8 : 4)) fold_kernel(const FoldArgs a) {
     constexpr int NPAR = kFoldThreads / kFoldNJ;   // token parities per B row
-    static_assert(!RAW || kFoldNJ == 32, "mode ii: 4 warps x 8 d_v rows (one MMA n-tile each)");
     const int jh = blockIdx.x, h = blockIdx.y, zi = blockIdx.z;
     if constexpr (PG) {   // slot lists, state indices and block tables may come from the previous grid
         if (a.pdl) pdl_wait();
@@ -85,7 +69,7 @@ __global__ void __launch_bounds__(kFoldThreads, RAW ? 4 : (kFoldNJ == 128 ? 2 : 
     const int KC = a.kc;                           // staging chunk (multiple of 8, <= 32)
 
     extern __shared__ __align__(1024) unsigned char smem[];
-    const FoldSmem L = fold_smem_layout(FP32_IN, kFoldNJ, KC, RAW ? a.kcap : 0);
+    const FoldSmem L = fold_smem_layout(FP32_IN, kFoldNJ, KC);
     float *S_s = reinterpret_cast<float *>(smem + L.S);
     unsigned char *A = smem + L.A, *Alo = smem + L.Alo, *Bhi = smem + L.Bhi, *Blo = smem + L.Blo;
     uint64_t *bar_ld = reinterpret_cast<uint64_t *>(smem + L.bar);
@@ -135,23 +119,12 @@ __global__ void __launch_bounds__(kFoldThreads, RAW ? 4 : (kFoldNJ == 128 ? 2 : 
     float kv[KCM], uv[KCM / NPAR], gv[KCM / NPAR];
     auto load_chunk = [&](int kc0, int kn) {
 #pragma unroll
-        for (int i = 0; i < KCM; ++i) {
-            if constexpr (RAW)
-                kv[i] = (i < kn) ? reinterpret_cast<const float *>(smem + L.Ks)[(kc0 + i) * kKs + c] : 0.f;
-            else
-                kv[i] = (i < kn) ? to_f(Kp(kc0 + i)[c]) : 0.f;
-        }
+        for (int i = 0; i < KCM; ++i) kv[i] = (i < kn) ? to_f(Kp(kc0 + i)[c]) : 0.f;
 #pragma unroll
         for (int q = 0; q < KCM / NPAR; ++q) {
             const int i = NPAR * q + ip;
-            if constexpr (RAW)
-                uv[q] = (i < kn) ? reinterpret_cast<const float *>(smem + L.Us)[(kc0 + i) * kFoldNJ + jb] : 0.f;
-            else
-                uv[q] = (i < kn) ? to_f(*Up(kc0 + i)) : 0.f;
-            if constexpr (RAW)
-                gv[q] = (i < kn) ? reinterpret_cast<const float *>(smem + L.Gs)[kc0 + i] : 0.f;
-            else
-                gv[q] = (i < kn) ? a.p.G[rec(kc0 + i)] : 0.f;
+            uv[q] = (i < kn) ? to_f(*Up(kc0 + i)) : 0.f;
+            gv[q] = (i < kn) ? a.p.G[rec(kc0 + i)] : 0.f;
         }
     };
 
@@ -213,33 +186,7 @@ __global__ void __launch_bounds__(kFoldThreads, RAW ? 4 : (kFoldNJ == 128 ? 2 : 
             bulk_g2s(S_s, state_tile, kFoldNJ * kD * 4, bar_ld);
         }
     }
-    if constexpr (RAW) {
-        // raw records of every token this launch may fold, requested in
-        // batches of 16 loads per thread: keys -> fp32 rows, log decays, betas,
-        // and the thread's raw values v_i[j] (parked in Us)
-        float *Ks = reinterpret_cast<float *>(smem + L.Ks);
-        float *Gs = reinterpret_cast<float *>(smem + L.Gs);
-        float *Bs = reinterpret_cast<float *>(smem + L.Bs);
-        float *Us = reinterpret_cast<float *>(smem + L.Us);
-        for (int i0 = 0; i0 < a.kcap; i0 += 16) {
-            float t[16];
-#pragma unroll
-            for (int u = 0; u < 16; ++u) t[u] = (i0 + u < a.kcap) ? to_f(Kp(i0 + u)[c]) : 0.f;
-#pragma unroll
-            for (int u = 0; u < 16; ++u) Ks[(i0 + u) * kKs + c] = t[u];
-        }
-        for (int i0 = ip; i0 < a.kcap; i0 += 16 * NPAR) {
-            float t[16];
-#pragma unroll
-            for (int u = 0; u < 16; ++u) {
-                const int i = i0 + NPAR * u;
-                t[u] = (i < a.kcap) ? to_f(static_cast<const InT *>(a.p.V)[rec(i) * kD + jr]) : 0.f;
-            }
-#pragma unroll
-            for (int u = 0; u < 16; ++u) if (i0 + NPAR * u < a.kcap) Us[(i0 + NPAR * u) * kFoldNJ + jb] = t[u];
-        }
-        for (int i = tid; i < a.kcap; i += kFoldThreads) { Gs[i] = a.p.G[rec(i)]; Bs[i] = a.p.B[rec(i)]; }
-    } else if (a.kind != FK_BRANCH) {
+    if (a.kind != FK_BRANCH) {
         load_chunk(0, min(KC, a.kcap));
     }
     tc_fence_before();
@@ -250,126 +197,13 @@ __global__ void __launch_bounds__(kFoldThreads, RAW ? 4 : (kFoldNJ == 128 ? 2 : 
     if (a.kind == FK_BRANCH) {   // the record remap needs the counters: load after them
         bocc = meta[2];
         boff = meta[3];
-        if constexpr (!RAW) load_chunk(0, min(KC, n));
+        load_chunk(0, min(KC, n));
     }
     const uint32_t tmem = *tmem_slot;
     if (n == 0) {   // nothing to fold: state untouched, counters unchanged
         if (a.spec) mbar_wait(bar_ld, 0);   // the speculative copy must land before exit
         if (warp == 0) tmem_dealloc<kFoldNJ>(tmem);
         return;
-    }
-    if constexpr (RAW) {
-        const float *Ks = reinterpret_cast<const float *>(smem + L.Ks);
-        const float *Gs = reinterpret_cast<const float *>(smem + L.Gs);
-        const float *Bs = reinterpret_cast<const float *>(smem + L.Bs);
-        float *Gm = reinterpret_cast<float *>(smem + L.Gm);
-        float *Us = reinterpret_cast<float *>(smem + L.Us);
-        const int lane = tid & 31;
-        // (1) scaled strictly-lower Gram matrix  Gm[i][l] = beta_i e^{G_i-G_l} (k_i.k_l), l < i;
-        //     one thread per pair (pairs enumerated row by row), rotated 16-byte
-        //     chunks so the 8 lanes of a shared-memory phase hit distinct bank groups
-        {
-            const int npair = n * (n - 1) / 2;
-            for (int p = tid; p < npair; p += kFoldThreads) {
-                int i = (int)((1.f + sqrtf(1.f + 8.f * (float)p)) * 0.5f);
-                while (i * (i - 1) / 2 > p) --i;
-                while ((i + 1) * i / 2 <= p) ++i;
-                const int l = p - i * (i - 1) / 2;
-                float acc0 = 0.f, acc1 = 0.f;
-#pragma unroll 8
-                for (int cc = 0; cc < kD / 4; cc += 2) {
-                    const int c0 = (cc + lane) & (kD / 4 - 1), c1 = (cc + 1 + lane) & (kD / 4 - 1);
-                    const float4 x0 = *reinterpret_cast<const float4 *>(Ks + i * kKs + 4 * c0);
-                    const float4 y0 = *reinterpret_cast<const float4 *>(Ks + l * kKs + 4 * c0);
-                    const float4 x1 = *reinterpret_cast<const float4 *>(Ks + i * kKs + 4 * c1);
-                    const float4 y1 = *reinterpret_cast<const float4 *>(Ks + l * kKs + 4 * c1);
-                    acc0 = fmaf(x0.x, y0.x, fmaf(x0.y, y0.y, fmaf(x0.z, y0.z, fmaf(x0.w, y0.w, acc0))));
-                    acc1 = fmaf(x1.x, y1.x, fmaf(x1.y, y1.y, fmaf(x1.z, y1.z, fmaf(x1.w, y1.w, acc1))));
-                }
-                Gm[i * n + l] = Bs[i] * expf(Gs[i] - Gs[l]) * (acc0 + acc1);
-            }
-        }
-        // (2) right-hand side  Us[i][j] = beta_i (v_i[j] - e^{G_i} W[i][j]),  W = K S0^T on the
-        //     warp-level tensor cores: W^T tile [16 tokens x 8 rows] per (m-tile, warp) =
-        //     K [tokens x 128] . S0^T [128 x rows] (mma.sync m16n8k8 tf32; bf16 keys exact,
-        //     S0 split hi + lo; fp32 keys split too); A = the padded key rows by ldmatrix
-        if (!zero_s0) {
-            mbar_wait(bar_ld, 0);
-            const int g = lane >> 2, t4 = lane & 3, lr = lane & 7, lm = lane >> 3;
-            const float *srow = S_s + (size_t)(warp * 8 + g) * kD;     // B: S0 row 8 warp + g
-            for (int mt = 0; mt < (n + 15) / 16; ++mt) {
-                float acc[4] = {0.f, 0.f, 0.f, 0.f};
-                const uint32_t ab = smem_u32(Ks) + (uint32_t)(((mt * 16 + lr + (lm & 1) * 8) * kKs + (lm >> 1) * 4) * 4);
-#pragma unroll 4
-                for (int kk = 0; kk < kD / 8; ++kk) {
-                    uint32_t ka[4];
-                    ldsm_x4(ka, ab + kk * 32);
-                    const float s0 = srow[kk * 8 + t4], s1 = srow[kk * 8 + t4 + 4];
-                    const uint32_t h0 = __float_as_uint(s0) & 0xFFFFE000u, h1 = __float_as_uint(s1) & 0xFFFFE000u;
-                    const uint32_t l0 = __float_as_uint(s0 - __uint_as_float(h0));
-                    const uint32_t l1 = __float_as_uint(s1 - __uint_as_float(h1));
-                    if constexpr (FP32_IN) {
-                        uint32_t khi[4], klo[4];
-#pragma unroll
-                        for (int q = 0; q < 4; ++q) {
-                            khi[q] = ka[q] & 0xFFFFE000u;
-                            klo[q] = __float_as_uint(__uint_as_float(ka[q]) - __uint_as_float(khi[q]));
-                        }
-                        mma_tf32_16x8x8(acc, khi, h0, h1);
-                        mma_tf32_16x8x8(acc, khi, l0, l1);
-                        mma_tf32_16x8x8(acc, klo, h0, h1);
-                    } else {
-                        mma_tf32_16x8x8(acc, ka, h0, h1);   // bf16 keys are exact in tf32
-                        mma_tf32_16x8x8(acc, ka, l0, l1);
-                    }
-                }
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const int i = mt * 16 + g + (q >> 1) * 8, j = warp * 8 + 2 * t4 + (q & 1);
-                    if (i < n) Us[i * kFoldNJ + j] = Bs[i] * (Us[i * kFoldNJ + j] - expf(Gs[i]) * acc[q]);
-                }
-            }
-        } else {   // compression: S0 = 0, W = 0
-            for (int i = ip; i < n; i += NPAR) Us[i * kFoldNJ + jb] = Bs[i] * Us[i * kFoldNJ + jb];
-        }
-        __syncthreads();
-        // (3) forward substitution down each column (lane = d_v row of the tile);
-        //     up to 32 tokens the column lives in registers and each row's sum
-        //     runs on two accumulator chains (Gm reads are warp broadcasts)
-        if (warp == 0) {
-            if (n <= 32) {
-                float u[32];
-#pragma unroll
-                for (int i = 0; i < 32; ++i) u[i] = i < n ? Us[i * kFoldNJ + lane] : 0.f;
-#pragma unroll
-                for (int i = 1; i < 32; ++i) {
-                    if (i < n) {
-                        float x0 = u[i], x1 = 0.f;
-#pragma unroll
-                        for (int l = 0; l < i; l += 2) {
-                            x0 = fmaf(-Gm[i * n + l], u[l], x0);
-                            if (l + 1 < i) x1 = fmaf(-Gm[i * n + l + 1], u[l + 1], x1);
-                        }
-                        u[i] = x0 + x1;
-                    }
-                }
-#pragma unroll
-                for (int i = 0; i < 32; ++i) if (i < n) Us[i * kFoldNJ + lane] = u[i];
-            } else {
-                for (int i = 1; i < n; ++i) {
-                    float x0 = Us[i * kFoldNJ + lane], x1 = 0.f;
-                    int l = 0;
-                    for (; l + 1 < i; l += 2) {
-                        x0 = fmaf(-Gm[i * n + l], Us[l * kFoldNJ + lane], x0);
-                        x1 = fmaf(-Gm[i * n + l + 1], Us[(l + 1) * kFoldNJ + lane], x1);
-                    }
-                    if (l < i) x0 = fmaf(-Gm[i * n + l], Us[l * kFoldNJ + lane], x0);
-                    Us[i * kFoldNJ + lane] = x0 + x1;
-                }
-            }
-        }
-        __syncthreads();
-        load_chunk(0, min(KC, n));
     }
     const float g_last = __int_as_float(meta[4]);
     const uint32_t idesc = idesc_tf32(128, kFoldNJ);
@@ -469,11 +303,11 @@ __global__ void __launch_bounds__(kFoldThreads, RAW ? 4 : (kFoldNJ == 128 ? 2 : 
     }
 }
 
-template <typename InT, typename UT, bool FP32_IN, int NJ, int KCM, bool RAW>
+template <typename InT, typename UT, bool FP32_IN, int NJ, int KCM>
 static cudaError_t launch_fold_cfg(const FoldArgs &a, cudaStream_t s) {
-    const FoldSmem L = fold_smem_layout(FP32_IN, NJ, a.kc, RAW ? a.kcap : 0);
+    const FoldSmem L = fold_smem_layout(FP32_IN, NJ, a.kc);
     const bool pg = a.slots || a.p.btab || a.p.sidx;
-    auto kfn = pg ? fold_kernel<InT, UT, FP32_IN, NJ, KCM, RAW, true> : fold_kernel<InT, UT, FP32_IN, NJ, KCM, RAW, false>;
+    auto kfn = pg ? fold_kernel<InT, UT, FP32_IN, NJ, KCM, true> : fold_kernel<InT, UT, FP32_IN, NJ, KCM, false>;
     cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
     if (e != cudaSuccess) return e;
     // the whole L1 / shared carveout for shared memory: CTAs per SM are bounded
@@ -492,9 +326,8 @@ static cudaError_t launch_fold_t(const FoldArgs &a, cudaStream_t s) {
     // take 64-row CTAs (half the CTAs): config-3 commit 164 -> 127 us.  Full
     // flushes keep 32-row CTAs (more CTAs per SM in flight): 57 vs 62 us.
     const int nj = a.spec ? 32 : 64;
-    if (a.raw) return launch_fold_cfg<InT, UT, FP32_IN, 32, kFoldKCMax, true>(a, s);
-    if (nj == 64) return launch_fold_cfg<InT, UT, FP32_IN, 64, kFoldKCMax, false>(a, s);
-    return launch_fold_cfg<InT, UT, FP32_IN, 32, kFoldKCMax, false>(a, s);
+    if (nj == 64) return launch_fold_cfg<InT, UT, FP32_IN, 64, kFoldKCMax>(a, s);
+    return launch_fold_cfg<InT, UT, FP32_IN, 32, kFoldKCMax>(a, s);
 }
 
 cudaError_t launch_fold(const FoldArgs &a_in, cudaStream_t s, int64_t *launches) {
@@ -510,7 +343,9 @@ cudaError_t launch_fold(const FoldArgs &a_in, cudaStream_t s, int64_t *launches)
     // flush against 32-token chunks at 4 CTAs/SM.
     a.kc = kc < 8 ? 8 : (kc > kFoldKCMax ? kFoldKCMax : kc);
     cudaError_t e;
-    if (a.dm.in_dt == DT_F32)
+    if (a.raw)
+        e = launch_fold_ut(a, s);
+    else if (a.dm.in_dt == DT_F32)
         e = launch_fold_t<float, float, true>(a, s);
     else if (a.dm.u_dt == DT_F16)
         e = launch_fold_t<__nv_bfloat16, __half, false>(a, s);

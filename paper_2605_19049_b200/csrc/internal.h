@@ -116,6 +116,7 @@ struct FoldArgs {
     int fork_n = 0, fork_dst = -1;  // FK_FORK
     const int *branch = nullptr;    // FK_BRANCH: accepted branch per slot
     int n_branch = 1;               // FK_BRANCH: branches of n_draft drafts
+    const void *tmap = nullptr;     // raw (mode ii): host CUtensorMap of the state (see ChunkArgs::tmap)
 };
 cudaError_t launch_commit_append(const Dims &dm, const Ptrs &p, int first, int n, const int *nacc, int n_draft,
                                  int pdl, cudaStream_t s, int64_t *launches);
@@ -136,6 +137,8 @@ struct RecArgs {
 // Launchers: return cudaSuccess or the launch error; *launches += kernels.
 cudaError_t launch_chunk(const ChunkArgs &a, cudaStream_t s, int64_t *launches);
 cudaError_t launch_fold(const FoldArgs &a, cudaStream_t s, int64_t *launches);
+// mode ii (fold_ut.cu): one CTA of 8 warps per (V head, slot); FULL / FORCE only
+cudaError_t launch_fold_ut(const FoldArgs &a, cudaStream_t s);
 cudaError_t launch_recurrent_step(const RecArgs &a, cudaStream_t s, int64_t *launches);
 cudaError_t launch_recurrent_verify(const RecArgs &a, cudaStream_t s, int64_t *launches);
 cudaError_t launch_recurrent_commit(const RecArgs &a, cudaStream_t s, int64_t *launches);

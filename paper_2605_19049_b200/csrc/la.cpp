@@ -655,6 +655,7 @@ la_status la_flush(la_buf *b, int32_t first, int32_t n, int32_t kind, la_stream 
     a.dm = b->dm; a.p = b->p; a.first = first; a.n = n;
     a.kind = kind == LA_FLUSH_FULL ? FK_FULL : FK_FORCE; a.nacc = nullptr; a.n_draft = 0; a.kcap = kcap; a.spec = all;
     a.raw = raw ? 1 : 0;
+    if (raw && !(a.tmap = state_tmap(b))) return fail(LA_ERR_CUDA, "no tensor map for the state (driver entry point missing)");
     std::lock_guard<std::mutex> lk(g_enqueue_mu);
     Stage stg;
     if (kind == LA_FLUSH_FORCE)
