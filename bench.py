@@ -776,8 +776,9 @@ def extra_rows(torch, L, cost, dev, stream, seed, K, W, peak, args):
         "us_per_launch": raw_us, "bytes_per_launch": raw_bytes,
         "gbs": gbs(raw_bytes, raw_us), "frac_of_measured": gbs(raw_bytes, raw_us) / peak,
         "mode_i_us_per_launch_same_buffers": ui_us,
-        "note": "UT transform in the flush: W = K S0^T and the Gram matrix on CUDA cores, C x C forward "
-                "substitution in shared memory, then the split-TF32 tcgen05 fold (P:392-399, reading Z4)",
+        "note": "UT transform in the flush (P:392-399, reading Z4): Gram K K^T, A = (I + L)^-1 by forward "
+                "substitution, V~ = A Diag(beta) V before the state lands; U = V~ - Q (K S0^T) and the fold on "
+                "split-TF32 mma.sync, one 8-warp CTA per (head, slot) (csrc/fold_ut.cu)",
     }
     del gd2, gr2, gd2b, gi2, bufs, xs2
     torch.cuda.synchronize()
