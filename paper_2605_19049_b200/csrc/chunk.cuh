@@ -213,6 +213,27 @@ constexpr int kFusedFoldMaxC = 32;
 // new tokens from which the state mat-vecs run on the tensor cores
 constexpr int kTcMinTokens = 8;
 
+#ifdef LABUF_CK_PROF
+// per-CTA timeline of the last chunk-kernel launch (globaltimer ns, SM id):
+// entry, state + tokens landed, records landed, exit -- tools/ck_prof.py
+__device__ unsigned long long g_ck_prof[8192][5];
+__device__ __forceinline__ unsigned long long ck_now() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define CK_MARK(i)                                                                                   \
+    do {                                                                                             \
+        const int cta_ = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);             \
+        if (threadIdx.x == 0 && cta_ < 8192) {                                                       \
+            g_ck_prof[cta_][i] = ck_now();                                                           \
+            if (i == 0) { unsigned sm_; asm("mov.u32 %0, %%smid;" : "=r"(sm_)); g_ck_prof[cta_][4] = sm_; } \
+        }                                                                                            \
+    } while (0)
+#else
+#define CK_MARK(i) do { } while (0)
+#endif
+
 template <typename InT, typename UT, int TPC, int WPT, int NT, bool HAS_STATE, int MINB, bool TC, bool FOLD = false,
           bool MMA = false, bool PG = false>
 __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const ChunkArgs a,
@@ -234,6 +255,7 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
     static_assert(NTHR >= 64, "warp 0 requests the records, warp 1 the new tokens");
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    CK_MARK(0);
     const int seg = lane & 3, team = lane >> 2, par = team & 1;
     const int wt = warp / WPT, half = warp % WPT;  // the warp's d_v tile and row block in it
     const Dims dm = a.dm;
@@ -388,7 +410,8 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
             mbar_arrive_expect_tx(full, fixed_bytes);
             if (HAS_STATE) issue_state();
         }
-        const int j0v = (direct ? a.p.len : a.p.occ)[r] + a.j_add;
+        // (host-exact uniform count: the records are requested without the counter round trip)
+        const int j0v = a.j0_fixed >= 0 ? a.j0_fixed : (direct ? a.p.len : a.p.occ)[r] + a.j_add;
         const int jbv = (j0v + 3) & ~3;
         *j0_s = j0v;
         mbar_arrive_expect_tx(recs, (uint32_t)(TPC * 32 * j0v * usz) + (uint32_t)(j0v * kD * isz) +
@@ -440,6 +463,7 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
         if (lane % segl >= off) x_l += y;
     }
     mbar_wait(tokb, 0);   // (non-MMA kinds: tokb == full, the state and the tokens)
+    CK_MARK(1);
     // multi-token launches read k_t / q_t once per row step: widen them to
     // fp32 once per CTA ([t][k | q][128])
     // (with the warp-MMA pass the fp32 B rows double as the widened k_t / q_t)
@@ -641,6 +665,7 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
         }
         // ---- the buffered records: j0, log decays
         mbar_wait(recs, 0);
+        CK_MARK(2);
         j0 = *j0_s;
         J = j0 + n_new;
         gn_l = (j0 > 0 ? G_s[j0 - 1] : 0.f) + x_l;
@@ -1082,6 +1107,7 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
         else a.p.occ[r] = (FOLD && J == dm.C) ? 0 : J;
     }
     if (bad) atomicOr(a.p.status, bad);
+    CK_MARK(3);
     if constexpr (FOLD) {
         if (J == dm.C && tid == 0) bulk_wait_read0();   // shared memory stays live until the store has read it
     }

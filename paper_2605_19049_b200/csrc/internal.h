@@ -74,6 +74,9 @@ struct ChunkArgs {
     int n_new;          // tokens processed per slot in this launch (<= kMaxNewPerLaunch)
     int j0_cap;         // max over the range of the buffered count j0 (sizes smem)
     int j_add;          // added to the device count (verify split into several launches)
+    int j0_fixed = -1;  // >= 0: every slot of the (contiguous) range holds exactly this many
+                        // records (host mirror exact): the kernel requests them at once
+                        // instead of reading the device counter first
     int seg = 0;        // branch verify: new tokens form independent branches of `seg` tokens
                         // (causal and cumulative decay only within a branch); 0 = one sequence
     int tok_total;      // tokens per slot in the caller's q/k/v/alpha/beta/o arrays

@@ -235,6 +235,12 @@ la_status check_chunkwise(la_buf *b, int r) {
     if (b->sidx[r] < 0) return fail(LA_ERR_MODE, "slot %d holds no state (reset it as CHUNKWISE)", r);
     return LA_OK;
 }
+// every slot of [first, first + n) holds exactly the same, exactly known count
+bool uniform_exact(const la_buf *b, int first, int n, const std::vector<int> &cnt) {
+    for (int r = first; r < first + n; ++r)
+        if (b->occ_ub[r] || cnt[r] != cnt[first]) return false;
+    return n > 0;
+}
 // calls that need the exact occupancy (decode, FULL flush, prefill, mixed, recurrent)
 la_status check_exact(la_buf *b, int r) {
     if (b->occ_ub[r])
@@ -271,7 +277,8 @@ la_status set_device(la_buf *b) {
 cudaError_t run_chunk(la_buf *b, int first, int n, int n_tok, int j0_cap, int tok_base, int tok_total,
                       int kind, const void *q, const void *k, const void *v, const float *alpha,
                       const float *beta, float *o, cudaStream_t s, int fold = 0,
-                      const int *slots = nullptr, const int *pos = nullptr, int passes = 3, int seg = 0) {
+                      const int *slots = nullptr, const int *pos = nullptr, int passes = 3, int seg = 0,
+                      bool j0_uniform = false) {
     const int mx = max_new_per_launch(b->dm.g);
     const size_t isz = dt_size(b->cfg.in_dtype);
     const size_t d = kD;
@@ -288,6 +295,7 @@ cudaError_t run_chunk(la_buf *b, int first, int n, int n_tok, int j0_cap, int to
                 a.dm = b->dm; a.p = b->p;
                 a.first = first + s0; a.n = std::min(kMaxSlotsPerLaunch, n - s0);
                 a.n_new = m; a.j0_cap = j0_cap + off;
+                a.j0_fixed = (j0_uniform && !slots) ? j0_cap + off : -1;
                 a.j_add = (kind == CK_VERIFY) ? off : 0;
                 a.tok_total = tok_total; a.tok_offset = tok_base + off; a.kind = kind;
                 const size_t sq = slots ? 0 : (size_t)s0 * tok_total;          // token rows skipped
@@ -603,13 +611,15 @@ la_status la_decode_step(la_buf *b, int32_t first, int32_t n, const void *q, con
     if ((st = check_blocks(b, g)) != LA_OK) return st;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     std::lock_guard<std::mutex> lk(g_enqueue_mu);
+    const bool uni = uniform_exact(b, first, n, b->occ);
     cudaError_t e = run_chunk(b, first, n, 1, j0_cap, 0, 1, CK_DECODE, q, k, v, alpha, beta, o, s, fold,
-                              nullptr, nullptr, 1);
+                              nullptr, nullptr, 1, 0, uni);
     if (e != cudaSuccess) return cuda_fail(e, "decode launch configuration");
     Stage stg;
     take_blocks(b, g, stg);
     if ((e = run_stage(b, stg, s)) != cudaSuccess) return cuda_fail(e, "stage launch");
-    e = run_chunk(b, first, n, 1, j0_cap, 0, 1, CK_DECODE, q, k, v, alpha, beta, o, s, fold, nullptr, nullptr, 2);
+    e = run_chunk(b, first, n, 1, j0_cap, 0, 1, CK_DECODE, q, k, v, alpha, beta, o, s, fold, nullptr, nullptr, 2, 0,
+                  uni);
     if (e != cudaSuccess) return cuda_fail(e, "decode launch");
     for (int r = first; r < first + n; ++r) {
         b->occ[r] += 1;
@@ -701,14 +711,15 @@ la_status la_verify_drafts(la_buf *b, int32_t first, int32_t n, int32_t n_draft,
     if ((st = check_blocks(b, g)) != LA_OK) return st;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     std::lock_guard<std::mutex> lk(g_enqueue_mu);
+    const bool uni = uniform_exact(b, first, n, b->occ);
     cudaError_t e = run_chunk(b, first, n, n_draft, j0_cap, 0, n_draft, CK_VERIFY, q, k, v, alpha, beta, o, s, 0,
-                              nullptr, nullptr, 1);
+                              nullptr, nullptr, 1, 0, uni);
     if (e != cudaSuccess) return cuda_fail(e, "verify launch configuration");
     Stage stg;
     take_blocks(b, g, stg);
     if ((e = run_stage(b, stg, s)) != cudaSuccess) return cuda_fail(e, "stage launch");
     e = run_chunk(b, first, n, n_draft, j0_cap, 0, n_draft, CK_VERIFY, q, k, v, alpha, beta, o, s, 0,
-                  nullptr, nullptr, 2);
+                  nullptr, nullptr, 2, 0, uni);
     if (e != cudaSuccess) return cuda_fail(e, "verify launch");
     for (int r = first; r < first + n; ++r) b->pending[r] = n_draft;
     return LA_OK;
@@ -869,13 +880,15 @@ la_status la_direct_short(la_buf *b, int32_t first, int32_t n, int32_t n_new, co
     if ((st = check_blocks(b, g)) != LA_OK) return st;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     std::lock_guard<std::mutex> lk(g_enqueue_mu);
+    const bool uni = uniform_exact(b, first, n, b->len);
     cudaError_t e = run_chunk(b, first, n, n_new, j0_cap, 0, n_new, CK_DIRECT, q, k, v, alpha, beta, o, s, 0,
-                              nullptr, nullptr, 1);
+                              nullptr, nullptr, 1, 0, uni);
     if (e != cudaSuccess) return cuda_fail(e, "direct launch configuration");
     Stage stg;
     take_blocks(b, g, stg);
     if ((e = run_stage(b, stg, s)) != cudaSuccess) return cuda_fail(e, "stage launch");
-    e = run_chunk(b, first, n, n_new, j0_cap, 0, n_new, CK_DIRECT, q, k, v, alpha, beta, o, s, 0, nullptr, nullptr, 2);
+    e = run_chunk(b, first, n, n_new, j0_cap, 0, n_new, CK_DIRECT, q, k, v, alpha, beta, o, s, 0, nullptr, nullptr, 2,
+                  0, uni);
     if (e != cudaSuccess) return cuda_fail(e, "direct launch");
     for (int r = first; r < first + n; ++r) b->len[r] += n_new;
     return LA_OK;

@@ -1,0 +1,45 @@
+"""Per-CTA timeline of one config-2 decode launch (batch 64, C = 16, bf16,
+occupancy j after warm-up) from a -DLABUF_CK_PROF build:
+    LABUF_LIB=ab/liblabuf_ckprof.so python tools/ck_prof.py [j]
+Prints the launch span, per-phase latency percentiles and the CTAs resident
+per SM over time."""
+import ctypes
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+
+import synth.device as sd
+from paper_2605_19049_b200 import labuf as L
+
+B, C, Hk, Hv = 64, 16, 16, 32
+j = int(sys.argv[1]) if len(sys.argv) > 1 else 8
+bufs = [L.LaBuf(L.make_config(B, Hk, Hv, chunk=C), device="cuda") for _ in range(4)]
+for i, b in enumerate(bufs):
+    b.reset(zero_state=False)
+    b.state.copy_(sd.state0(i, B, Hv))
+xs = [sd.tokens(10 + t, B, 1, Hk, Hv, squeeze=True) for t in range(C)]
+o = torch.empty(B, Hv, 128, device="cuda")
+for t in range(j + 1):   # the last launch runs at occupancy j (4 handles rotated: L2 holds none of the state)
+    for b in bufs:
+        b.decode_step(0, xs[t]["q"], xs[t]["k"], xs[t]["v"], xs[t]["alpha"], xs[t]["beta"], o)
+torch.cuda.synchronize()
+lib = ctypes.CDLL(os.environ["LABUF_LIB"])
+raw = (ctypes.c_ulonglong * (8192 * 5))()
+assert lib.la_debug_ck_prof(raw) == 0
+a = np.frombuffer(raw, dtype=np.uint64).reshape(8192, 5)[: B * Hv * 2].astype(np.int64)
+t0 = a[:, 0].min()
+st, land, recs, end, sm = a[:, 0] - t0, a[:, 1] - t0, a[:, 2] - t0, a[:, 3] - t0, a[:, 4]
+print(f"occupancy {j}: {len(a)} CTAs, span {end.max() / 1e3:.2f} us (first start 0, last start {st.max() / 1e3:.2f})")
+for name, x in (("load (state+tokens)", land - st), ("records after state", recs - land), ("compute after records", end - recs),
+                ("CTA life", end - st)):
+    p = np.percentile(x, [5, 50, 95]) / 1e3
+    print(f"  {name:24s} p5 {p[0]:.2f}  p50 {p[1]:.2f}  p95 {p[2]:.2f} us")
+# resident CTAs per SM, sampled every 0.5 us
+grid = np.arange(0, end.max(), 500)
+res = [(np.sum((st <= g) & (end > g)) / len(np.unique(sm))) for g in grid]
+print("  resident CTAs per SM every 0.5 us:", " ".join(f"{x:.1f}" for x in res))
+loading = [(np.sum((st <= g) & (land > g)) / len(np.unique(sm))) for g in grid]
+print("  CTAs waiting for the state per SM:  ", " ".join(f"{x:.1f}" for x in loading))
