@@ -215,8 +215,9 @@ constexpr int kTcMinTokens = 8;
 
 #ifdef LABUF_CK_PROF
 // per-CTA timeline of the last chunk-kernel launch (globaltimer ns, SM id):
-// entry, state + tokens landed, records landed, exit -- tools/ck_prof.py
-__device__ unsigned long long g_ck_prof[8192][5];
+// 0 entry, 1 tokens (+ state) landed, 2 records landed, 3 exit, 4 state landed (MMA kinds),
+// 5 state pass done, 6 before the substitution, 7 after it -- tools/ck_prof.py
+__device__ unsigned long long g_ck_prof[8192][9];
 __device__ __forceinline__ unsigned long long ck_now() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -227,7 +228,7 @@ __device__ __forceinline__ unsigned long long ck_now() {
         const int cta_ = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);             \
         if (threadIdx.x == 0 && cta_ < 8192) {                                                       \
             g_ck_prof[cta_][i] = ck_now();                                                           \
-            if (i == 0) { unsigned sm_; asm("mov.u32 %0, %%smid;" : "=r"(sm_)); g_ck_prof[cta_][4] = sm_; } \
+            if (i == 0) { unsigned sm_; asm("mov.u32 %0, %%smid;" : "=r"(sm_)); g_ck_prof[cta_][8] = sm_; } \
         }                                                                                            \
     } while (0)
 #else
@@ -715,7 +716,7 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
                         const bool isq = v & 1;
                         if (t < n_new && i < J) {
                             bool valid = isq ? (i <= j0 + t) : (i < j0 + t);
-                            if (i >= j0 && (i - j0) / segl != t / segl) valid = false;   // another branch
+                            if (a.seg > 0 && i >= j0 && (i - j0) / segl != t / segl) valid = false;   // another branch
                             const float cf = valid ? expf(Gn_s[t] - (i < j0 ? G_s[i] : Gn_s[i - j0])) * acc[q] : 0.f;
                             (isq ? Cq : Ck)[i * NTP + t] = cf;
                         }
@@ -746,7 +747,7 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
                 const float gnew = __shfl_sync(0xffffffffu, gn_l, inew < NT ? inew : 0);
                 if (xid[o] >= 0 && i < J && t < n_new) {
                     bool valid = isq ? (i <= j0 + t) : (i < j0 + t);
-                    if (i >= j0 && (i - j0) / segl != t / segl) valid = false;   // another branch
+                    if (a.seg > 0 && i >= j0 && (i - j0) / segl != t / segl) valid = false;   // another branch
                     float cf = 0.f;
                     if (valid) cf = expf(gt - (i < j0 ? G_s[i] : gnew)) * res[o];
                     (isq ? Cq : Ck)[i * NTP + t] = cf;
@@ -756,6 +757,7 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
     }
     if constexpr (MMA) {
         mbar_wait(full, 0);   // the state tile (TMA, swizzled)
+        CK_MARK(4);
         float (&acc)[2 / WPT][mma_nrows(NT) / 8][4] = macc;
         // warp-level tensor cores (mma.sync m16n8k8 tf32, fp32 accumulate):
         // D[32 rows x 2NT] = S0 tile [32 x 128] . [k_t | q_t] [128 x 2NT];
@@ -854,6 +856,7 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
             }
         }
     }
+    CK_MARK(5);
     if (dm.validate) {
         for (int e = tid; e < n_new * kD; e += NTHR) {
             const float kk = to_f(k_s[(e / kD) * TS + e % kD]), qq = to_f(q_s[(e / kD) * TS + e % kD]);
@@ -869,6 +872,7 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
         }
     }
 
+    CK_MARK(6);
     // ---- 3. forward substitution over the new tokens.  Lane -> d_v row
     //         (half * RPW + lane % RPW) of the warp's tile; the WPT lanes of a
     //         row split the buffered records by i % WPT and combine by shuffle.
@@ -882,6 +886,12 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
             return make_int2(__ldcg(a.p.btab + (size_t)r * dm.maxb + (j0 + t) / dm.bt), (j0 + t) % dm.bt);
         };
         float un[NT];
+        // per-token e^{G_t} (lane t computes it once; broadcast by shuffle) and
+        // the output / record addresses of token 0 (token t is a fixed stride on)
+        const float eg_l = expf(gn_l);
+        const size_t ostr = (size_t)Hv * kD;
+        float *const obase = a.o ? a.o + (tok_of(0) * Hv + h) * kD + drow : nullptr;
+        UT *const ubase = static_cast<UT *>(a.p.U) + ((((size_t)r * Hv + h) * (kD / kUSub) + tile) * dm.bt + j0) * kUSub + row;
         // records part of every token's sums, record-outer for several tokens:
         // each u_i is loaded once and the tokens' coefficients of record i come
         // in 16-byte loads
@@ -944,7 +954,7 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
                 }
                 const float vt = to_f(v_s[t * TPC * 32 + wt * 32 + row]);
                 const float bt = Bn_s[t];
-                const float eG = expf(Gn_s[t]);
+                const float eG = __shfl_sync(0xffffffffu, eg_l, t);
                 float u, o;
                 if constexpr (MMA) {
                     // (S0 k_t, S0 q_t) of this row from the fragment holder: lane
@@ -976,10 +986,11 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
                 o = fmaf(cq[(j0 + t) * NTP], un[t], o);
                 if (sub == 0) {
                     if (dm.validate && !isfinite(vt)) bad |= 0x4u;
-                    if (a.o) a.o[(tok_of(t) * Hv + h) * kD + drow] = o;
+                    if (obase) obase[t * ostr] = o;
                     const int2 rp = recpos(t);
                     const size_t bh = (size_t)rp.x * Hv + h;
-                    static_cast<UT *>(a.p.U)[((bh * (kD / kUSub) + tile) * dm.bt + rp.y) * kUSub + row] = us;
+                    if (!PG || !a.p.btab) ubase[t * kUSub] = us;   // (contiguous records: position j0 + t of slot r)
+                    else static_cast<UT *>(a.p.U)[((bh * (kD / kUSub) + tile) * dm.bt + rp.y) * kUSub + row] = us;
                     if (dm.keep_raw) {
                         static_cast<InT *>(a.p.V)[(bh * dm.bt + rp.y) * kD + drow] = v_s[t * TPC * 32 + wt * 32 + row];
                         if (tile == 0 && row == 0) a.p.B[bh * dm.bt + rp.y] = bt;
@@ -1075,6 +1086,7 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
             }
         }
     }
+    CK_MARK(7);
     // ---- 4. records: k_t once per QK head, G_t per V head (first tile group)
     if (tg == 0) {
         if constexpr (PG) {

@@ -12,6 +12,7 @@ out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-so
 rows = list(csv.reader(io.StringIO(out)))
 hdr = next(r for r in rows if r and r[0] == "Line No")
 iS = hdr.index("Warp Stall Sampling (All Samples)")
+iI = hdr.index("Instructions Executed") if "Instructions Executed" in hdr else None
 lines, tot = [], 0
 for r in rows[rows.index(hdr) + 1:]:
     if r and r[0] and r[0] != "Line No":
@@ -20,8 +21,9 @@ for r in rows[rows.index(hdr) + 1:]:
         except (ValueError, IndexError):
             continue
         tot += v
-        lines.append((v, r[0], r[1].strip()[:110]))
+        ins = r[iI] if iI is not None and iI < len(r) else ""
+        lines.append((v, r[0], r[1].strip()[:100], ins))
 lines.sort(reverse=True)
 print(f"total stall samples {tot}")
-for v, ln, src in lines[:top]:
-    print(f"{v:6d} {100 * v / max(tot, 1):5.1f}%  L{ln}: {src}")
+for v, ln, src, ins in lines[:top]:
+    print(f"{v:6d} {100 * v / max(tot, 1):5.1f}%  inst {ins:>10s}  L{ln}: {src}")
