@@ -11,8 +11,8 @@ for r in $(seq 1 $ROUNDS); do
     python - $OUT/$v$r.json "$v$r" <<'PY' >> $OUT/summary.txt
 import json,sys
 try:
-    d=json.loads(open(sys.argv[1]).read().strip().splitlines()[-1]); k=d["kernels"]; r=d.get("rows",{}); v=r.get("verify_commit",{}); x=r.get("direct",{}); m=r.get("flush_mode_ii",{})
-    print(sys.argv[2], "decode %.2f flush %.1f rec %.2f | us/tok %.2f | verify %.1f commit %.1f | direct %.1f | raw %.1f" % (k["decode"]["us_per_launch"], k["flush"]["us_per_launch"], k["recurrent_step"]["us_per_launch"], d["us_per_token"], v.get("verify_us",0), v.get("commit_us",0), x.get("us_per_step",0), m.get("us_per_launch",0)))
+    d=json.loads(open(sys.argv[1]).read().strip().splitlines()[-1]); k=d["kernels"]; r=d.get("rows",{}); v=r.get("verify_commit",{}); x=r.get("direct",{}); m=r.get("flush_mode_ii",{}); pf=r.get("prefill",{})
+    print(sys.argv[2], "decode %.2f flush %.1f rec %.2f | us/tok %.2f | verify %.1f commit %.1f | direct %.1f | raw %.1f | prefill %.0f us" % (k["decode"]["us_per_launch"], k["flush"]["us_per_launch"], k["recurrent_step"]["us_per_launch"], d["us_per_token"], v.get("verify_us",0), v.get("commit_us",0), x.get("us_per_step",0), m.get("us_per_launch",0), 1e3 * pf.get("ms", 0)))
 except Exception as e:
     print(sys.argv[2], "failed", e)
 PY
