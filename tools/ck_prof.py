@@ -16,7 +16,19 @@ import synth.device as sd
 from paper_2605_19049_b200 import labuf as L
 
 C, Hk, Hv = 16, 16, 32
-if len(sys.argv) > 2 and sys.argv[1] == "verify":
+reader = "la_debug_ck_prof"
+if len(sys.argv) > 2 and sys.argv[1] == "direct":   # config 4: batch 1024, context L0 -> L0 + 1
+    L0 = int(sys.argv[2])
+    B, reader = 1024, "la_debug_ck_prof_direct"
+    b4 = L.LaBuf(L.make_config(B, Hk, Hv, chunk=16, short_cap=128, u_dtype="f16"), device="cuda")
+    b4.reset(mode=L.LA_MODE_DIRECT, zero_state=False)
+    pre = sd.tokens(30, B, L0, Hk, Hv)
+    po = torch.empty(B, L0, Hv, 128, device="cuda")
+    b4.direct_short(0, pre["q"], pre["k"], pre["v"], pre["alpha"], pre["beta"], po)
+    x = sd.tokens(40, B, 1, Hk, Hv)
+    o = torch.empty(B, 1, Hv, 128, device="cuda")
+    b4.direct_short(0, x["q"], x["k"], x["v"], x["alpha"], x["beta"], o)
+elif len(sys.argv) > 2 and sys.argv[1] == "verify":
     N = int(sys.argv[2])
     B, j = 256, 0
     bufs = [L.LaBuf(L.make_config(B, Hk, Hv, chunk=C, max_drafts=N), device="cuda") for _ in range(2)]
@@ -48,7 +60,7 @@ if "LABUF_LIB" not in os.environ:   # (driver for an ncu capture of the same lau
     sys.exit(0)
 lib = ctypes.CDLL(os.environ["LABUF_LIB"])
 raw = (ctypes.c_ulonglong * (8192 * 9))()
-assert lib.la_debug_ck_prof(raw) == 0
+assert getattr(lib, reader)(raw) == 0
 a = np.frombuffer(raw, dtype=np.uint64).reshape(8192, 9).astype(np.int64)
 a = a[a[:, 0] > 0]
 a = a[a[:, 0] >= a[:, 0].max() - 10**6]   # the last launch
