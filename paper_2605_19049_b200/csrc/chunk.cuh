@@ -80,7 +80,11 @@ __host__ __device__ inline CtaLayout cta_layout(int TPC, int nt, bool has_state,
     // tools/probe_smem_align.cu -- and trap otherwise)
     L.S = o;  o = al128(o + (has_state ? (uint32_t)(TPC * 32 * kD * 4) + (tc ? 1024u : 0u) : 0u));
     L.U = o;  o = al128(o + (uint32_t)(TPC * 32 * jcap * usz));
-    L.K = o;  o = al128(o + (uint32_t)(jcap * kD * isz));
+    // (direct one-token step: the key rows arrive by 2-D TMA, 16-record boxes of
+    //  64 bf16 columns with the 128-byte swizzle -- 1 KiB aligned, whole boxes)
+    const bool ktma_ = !has_state && nt == 1 && isz == 2 && !mma && !tc;
+    if (ktma_) o = (o + 1023u) & ~1023u;
+    L.K = o;  o = al128(o + (uint32_t)((ktma_ ? (jcap + 15) / 16 * 16 : jcap) * kD * isz));
     L.Gs = o; o = al128(o + (uint32_t)(((jcap + 3) & ~3) * 4));
     // (key-rows MMA kinds: q_t, k_t land straight in the padded rows Ap)
     const bool krm_ = mma && isz == 2;
@@ -300,6 +304,9 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
     // new tokens' q_t / k_t rows: token t at q_s + t * TS (key-rows MMA kinds: rows
     // 2t + 1 / 2t of the padded bf16 operand Ap)
     constexpr bool KRM = MMA && isz == 2;
+    // direct one-token step on a contiguous handle: key rows by TMA + mma.sync
+    // (runtime: the host passes the key tensor map in `tmap`, a.tmapk != null)
+    constexpr bool KTMA = !HAS_STATE && NT == 1 && isz == 2 && !MMA && !TC && !PG;
     constexpr int TS = KRM ? 2 * kKp : kD;
     const InT *q_s = KRM ? reinterpret_cast<const InT *>(smem + L.Ap) + kKp : reinterpret_cast<const InT *>(smem + L.q);
     const InT *k_s = KRM ? reinterpret_cast<const InT *>(smem + L.Ap) : reinterpret_cast<const InT *>(smem + L.k);
@@ -415,15 +422,26 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
         const int j0v = a.j0_fixed >= 0 ? a.j0_fixed : (direct ? a.p.len : a.p.occ)[r] + a.j_add;
         const int jbv = (j0v + 3) & ~3;
         *j0_s = j0v;
-        mbar_arrive_expect_tx(recs, (uint32_t)(TPC * 32 * j0v * usz) + (uint32_t)(j0v * kD * isz) +
-                                        (j0v ? (uint32_t)(jbv * 4) : 0u));
+        const uint32_t kbytes = (KTMA && a.tmapk) ? (uint32_t)((j0v + 15) / 16 * 4096) : (uint32_t)(j0v * kD * isz);
+        mbar_arrive_expect_tx(recs, (uint32_t)(TPC * 32 * j0v * usz) + kbytes + (j0v ? (uint32_t)(jbv * 4) : 0u));
         if (j0v) {
             for (int x = 0; x < TPC; ++x)
                 bulk_g2s(smem + L.U + (size_t)x * j0v * kUSub * usz,
                          static_cast<const UT *>(a.p.U) + ((((size_t)r * Hv + h) * (kD / kUSub) + tile0 + x) * T) * kUSub,
                          (uint32_t)(j0v * kUSub * usz), recs);
-            bulk_g2s(smem + L.K, static_cast<const InT *>(a.p.K) + ((size_t)r * Hk + hk) * T * kD,
-                     (uint32_t)(j0v * kD * isz), recs);
+            if (KTMA && a.tmapk) {
+                // key rows as 16-record x 64-column boxes, 128-byte swizzle (conflict-
+                // free ldmatrix); rows past j0 are other records or zero fill (unused)
+                const int nb = (j0v + 15) / 16, jp = (a.j0_cap + 15) / 16 * 16;
+                const int row = (r * Hk + hk) * T;
+                for (int b = 0; b < nb; ++b) {
+                    tma_load_2d(smem + L.K + b * 2048, &tmap, 0, row + b * 16, recs);
+                    tma_load_2d(smem + L.K + jp * 128 + b * 2048, &tmap, 64, row + b * 16, recs);
+                }
+            } else {
+                bulk_g2s(smem + L.K, static_cast<const InT *>(a.p.K) + ((size_t)r * Hk + hk) * T * kD,
+                         (uint32_t)(j0v * kD * isz), recs);
+            }
             bulk_g2s(smem + L.Gs, a.p.G + ((size_t)r * Hv + h) * T, (uint32_t)(jbv * 4), recs);
         }
         if (a.kind != CK_VERIFY) ticket = atomicAdd(&a.p.ticket[r], 1);
@@ -722,6 +740,47 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
                         }
                     }
                 }
+            }
+        } else if (KTMA && a.tmapk) {
+            // key rows on the tensor cores: D[i][n] = k_i . vec_n (n = 0: k_t, 1: q_t),
+            // mma.sync m16n8k16 bf16 (products exact, fp32 accumulate); A = the
+            // swizzled key boxes by ldmatrix (conflict-free), B = the token rows
+            const int g = lane >> 2, t4 = lane & 3, lr = lane & 7, lm = lane >> 3;
+            const int jp = (a.j0_cap + 15) / 16 * 16;
+            const uint32_t kbase = smem_u32(K_s);
+            const float gt = __shfl_sync(0xffffffffu, gn_l, 0);
+            const InT *vrow = g == 0 ? k_s : q_s;
+            for (int mt = warp; mt * 16 < j0; mt += TPC * WPT) {
+                float acc[4] = {0.f, 0.f, 0.f, 0.f};
+                const int arow = mt * 16 + lr + (lm & 1) * 8;
+#pragma unroll
+                for (int kk = 0; kk < kD / 16; ++kk) {
+                    const int chunk = (kk & 3) * 2 + (lm >> 1);
+                    uint32_t av4[4];
+                    ldsm_x4(av4, kbase + (uint32_t)((kk >> 2) * jp * 128 + arow * 128 + ((chunk ^ (arow & 7)) << 4)));
+                    uint32_t b0 = 0u, b1 = 0u;
+                    if (g < 2) {
+                        b0 = *reinterpret_cast<const uint32_t *>(vrow + kk * 16 + 2 * t4);
+                        b1 = *reinterpret_cast<const uint32_t *>(vrow + kk * 16 + 8 + 2 * t4);
+                    }
+                    mma_bf16_16x8x16(acc, av4, b0, b1);
+                }
+                if (t4 == 0) {
+#pragma unroll
+                    for (int hf = 0; hf < 2; ++hf) {
+                        const int i = mt * 16 + g + 8 * hf;
+                        if (i < j0) {   // (rows past j0: other records or zero fill)
+                            const float w = expf(gt - G_s[i]);
+                            Ck[i * NTP] = w * acc[2 * hf];
+                            Cq[i * NTP] = w * acc[2 * hf + 1];
+                        }
+                    }
+                }
+            }
+            // the new token's own key (record j0): q_t . k_t, weight e^0
+            if (warp == TPC * WPT - 1) {
+                const float dqk = warp_sum(dot4(load4(k_s + 4 * lane), load4(q_s + 4 * lane)));
+                if (lane == 0) Cq[j0 * NTP] = dqk;
             }
         } else
         for (int ks = warp; ks < KS; ks += TPC * WPT) {
@@ -1147,6 +1206,7 @@ static cudaError_t launch_cfg(const ChunkArgs &a, cudaStream_t s) {
     if (e != cudaSuccess) return e;   // configuration check only (all-or-nothing pre-pass)
     CUtensorMap tm;
     if (TC || MMA) tm = *static_cast<const CUtensorMap *>(a.tmap);
+    else if (!HAS_STATE && a.tmapk) tm = *static_cast<const CUtensorMap *>(a.tmapk);   // (direct: the key records)
     else memset(&tm, 0, sizeof(tm));
     return launch_k(kfn, dim3(4 / TPC, a.dm.Hv, a.n), dim3(TPC * WPT * 32), L.bytes, s, a.pdl != 0, a, tm);
 }

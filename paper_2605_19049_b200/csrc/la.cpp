@@ -84,6 +84,8 @@ struct la_buf {
     int prefill_chunk = 0;                           // la_set_prefill_chunk (0: chunk)
     alignas(64) unsigned char tmap[128];             // CUtensorMap of the state (tensor-core pass)
     int tmap_state = 0;                              // 0 not built, 1 ok, 2 unavailable
+    alignas(64) unsigned char tmapk[128];            // CUtensorMap of the bf16 key records (direct step)
+    int tmapk_state = 0;
 };
 
 namespace {
@@ -122,6 +124,28 @@ const void *state_tmap(la_buf *b) {
         }
     }
     return b->tmap_state == 1 ? b->tmap : nullptr;
+}
+
+// The bf16 key records of a contiguous handle viewed as a 2-D tensor
+// [R*Hk*T rows][128], read in 16-row x 64-column boxes (128 B, 128-byte
+// swizzle): the conflict-free ldmatrix operand of the direct step's key rows
+// on the tensor cores.  Built once per handle, on first use.
+const void *key_tmap(la_buf *b) {
+    if (b->tmapk_state == 0) {
+        b->tmapk_state = 2;
+        if (b->paged || b->cfg.in_dtype != LA_DT_BF16) return nullptr;
+        if (auto enc = tmap_encoder()) {
+            const cuuint64_t dims[2] = {(cuuint64_t)kD, (cuuint64_t)b->dm.R * b->dm.Hk * b->dm.T};
+            const cuuint64_t strides[1] = {(cuuint64_t)kD * 2};
+            const cuuint32_t box[2] = {64, 16};
+            const cuuint32_t estr[2] = {1, 1};
+            if (enc(reinterpret_cast<CUtensorMap *>(b->tmapk), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, b->p.K, dims,
+                    strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
+                b->tmapk_state = 1;
+        }
+    }
+    return b->tmapk_state == 1 ? b->tmapk : nullptr;
 }
 
 // Launch overlap bookkeeping.  With programmatic dependent launch a kernel's
@@ -308,6 +332,7 @@ cudaError_t run_chunk(la_buf *b, int first, int n, int n_tok, int j0_cap, int to
                 a.slots = slots ? slots + s0 : nullptr;
                 a.pos = pos ? pos + s0 : nullptr;
                 a.tmap = (kind == CK_VERIFY || kind == CK_PREFILL) && m >= 2 ? state_tmap(b) : nullptr;
+                a.tmapk = (kind == CK_DIRECT && m == 1 && !slots) ? key_tmap(b) : nullptr;
                 a.fold = fold;
                 a.seg = seg;
                 a.dry = pass == 0;
