@@ -942,7 +942,8 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
         // record position j0 + t of the slot: (block, offset)
         auto recpos = [&](int t) -> int2 {
             if (!PG || !a.p.btab) return make_int2(r, j0 + t);
-            return make_int2(__ldcg(a.p.btab + (size_t)r * dm.maxb + (j0 + t) / dm.bt), (j0 + t) % dm.bt);
+            return make_int2(__ldcg(a.p.btab + (size_t)r * dm.maxb + (dm.bt_shift >= 0 ? (j0 + t) >> dm.bt_shift : (j0 + t) / dm.bt)),
+                                 dm.bt_shift >= 0 ? (j0 + t) & (dm.bt - 1) : (j0 + t) % dm.bt);
         };
         float un[NT];
         // per-token e^{G_t} (lane t computes it once; broadcast by shuffle) and
@@ -1151,7 +1152,8 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
         if constexpr (PG) {
             auto recpos = [&](int t) -> int2 {
                 if (!a.p.btab) return make_int2(r, j0 + t);
-                return make_int2(__ldcg(a.p.btab + (size_t)r * dm.maxb + (j0 + t) / dm.bt), (j0 + t) % dm.bt);
+                return make_int2(__ldcg(a.p.btab + (size_t)r * dm.maxb + (dm.bt_shift >= 0 ? (j0 + t) >> dm.bt_shift : (j0 + t) / dm.bt)),
+                                 dm.bt_shift >= 0 ? (j0 + t) & (dm.bt - 1) : (j0 + t) % dm.bt);
             };
             if (h % dm.g == 0) {
                 for (int idx = tid; idx < n_new * kD; idx += NTHR) {

@@ -28,6 +28,7 @@ struct Dims {
     int R, Hk, Hv, g, T, C;
     int in_dt, u_dt, keep_raw, validate;
     int bt, maxb;        // tokens per record block; blocks per slot (table row length)
+    int bt_shift;        // log2(bt) when bt is a power of two (block / offset by shift and mask), else -1
     int variant;         // 0 GDN (gate + delta rule), 1 gated LA (no delta), 2 vanilla LA
 };
 
@@ -55,6 +56,8 @@ struct Ptrs {
 // (block id, offset) of record position pos of slot r
 __device__ __forceinline__ int2 rec_at(const Dims &dm, const Ptrs &p, int r, int pos) {
     if (!p.btab) return make_int2(r, pos);
+    if (dm.bt_shift >= 0)   // (no integer division: the usual power-of-two block size)
+        return make_int2(p.btab[(size_t)r * dm.maxb + (pos >> dm.bt_shift)], pos & (dm.bt - 1));
     return make_int2(p.btab[(size_t)r * dm.maxb + pos / dm.bt], pos % dm.bt);
 }
 #endif

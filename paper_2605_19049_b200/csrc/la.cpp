@@ -536,6 +536,9 @@ la_status la_buf_create(const la_config *cfg, void *state, void *buffer, void *m
     b->occ_ub.assign(R, 0);
     b->branch_nd.assign(R, 0);
     dm.bt = b->sz.block_tokens; dm.maxb = b->sz.max_blocks;
+    dm.bt_shift = -1;
+    for (int sh = 0; sh < 31; ++sh)
+        if ((1 << sh) == dm.bt) dm.bt_shift = sh;
     dm.variant = cfg->variant;
     b->meta_i = m;
     b->i_sidx = b->sz.off_sidx / 4; b->i_btab = b->sz.off_btab / 4; b->i_wl = b->sz.off_wl / 4;
