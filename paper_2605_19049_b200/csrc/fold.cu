@@ -100,31 +100,33 @@ __global__ void __launch_bounds__(kFoldThreads, kFoldNJ == 128 ? 2 : (kFoldNJ ==
         const int ii = i >= bocc ? i + boff : i;
         return PG ? rec_at(dm, a.p, r, ii) : make_int2(r, ii);
     };
-    auto rec = [&](int i) -> size_t {   // (block * Hv + h) * bt + offset
-        const int2 ba = at(i);
-        return ((size_t)ba.x * Hv + h) * bt + ba.y;
-    };
-    auto Kp = [&](int i) {
-        const int2 ba = at(i);
-        return static_cast<const InT *>(a.p.K) + (((size_t)ba.x * dm.Hk + hk) * bt + ba.y) * kD;
-    };
-    auto Up = [&](int i) {
-        const int2 ba = at(i);
+    auto recb = [&](int2 ba) -> size_t { return ((size_t)ba.x * Hv + h) * bt + ba.y; };
+    auto rec = [&](int i) -> size_t { return recb(at(i)); };   // (block * Hv + h) * bt + offset
+    auto Kb = [&](int2 ba) { return static_cast<const InT *>(a.p.K) + (((size_t)ba.x * dm.Hk + hk) * bt + ba.y) * kD; };
+    auto Ub = [&](int2 ba) {
         return static_cast<const UT *>(a.p.U) +
                ((((size_t)ba.x * Hv + h) * (kD / kUSub) + jr / kUSub) * bt + ba.y) * kUSub + jr % kUSub;
     };
     // operands of one chunk: K^T column c, u_i[j], G_i — the first chunk is
     // requested at entry, bounded by the host's record count (in-capacity
-    // reads past a slot's own count are never used)
+    // reads past a slot's own count are never used).  Block tables: one lookup
+    // for the chunk's first record; the records that share its block (all of
+    // them for chunks of <= 16 inside 16-token blocks) are addressed from it
     float kv[KCM], uv[KCM / NPAR], gv[KCM / NPAR];
     auto load_chunk = [&](int kc0, int kn) {
+        // records kc0 .. kc0 + lim - 1 follow b0 in one block (a branch remap
+        // inside the chunk: every record through at())
+        const int2 b0 = at(kc0);
+        const int lim = (kc0 < bocc && kc0 + KCM > bocc) ? 0 : ((PG && a.p.btab) ? bt - b0.y : (1 << 30));
+        auto ba_of = [&](int i) -> int2 { return i < lim ? make_int2(b0.x, b0.y + i) : at(kc0 + i); };
 #pragma unroll
-        for (int i = 0; i < KCM; ++i) kv[i] = (i < kn) ? to_f(Kp(kc0 + i)[c]) : 0.f;
+        for (int i = 0; i < KCM; ++i) kv[i] = (i < kn) ? to_f(Kb(ba_of(i))[c]) : 0.f;
 #pragma unroll
         for (int q = 0; q < KCM / NPAR; ++q) {
             const int i = NPAR * q + ip;
-            uv[q] = (i < kn) ? to_f(*Up(kc0 + i)) : 0.f;
-            gv[q] = (i < kn) ? a.p.G[rec(kc0 + i)] : 0.f;
+            const int2 ba = ba_of(i);
+            uv[q] = (i < kn) ? to_f(*Ub(ba)) : 0.f;
+            gv[q] = (i < kn) ? a.p.G[recb(ba)] : 0.f;
         }
     };
 
