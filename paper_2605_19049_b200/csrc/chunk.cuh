@@ -244,8 +244,12 @@ template <typename InT, typename UT, int TPC, int WPT, int NT, bool HAS_STATE, i
 __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const ChunkArgs a,
                                                                         const __grid_constant__ CUtensorMap tmap) {
     static_assert(!TC || (HAS_STATE && TPC == 4 && WPT == 1), "tensor-core pass: whole head per CTA");
-    static_assert(!FOLD || (NT == 1 && HAS_STATE && WPT == 1 && !TC), "fused fold: decode kind only");
-    static_assert(!MMA || (HAS_STATE && (WPT == 1 || WPT == 2) && NT >= 2 && !TC && !FOLD),
+    // FOLD: the decode kind folds a filled buffer (NT = 1), or -- with MMA -- a
+    // prefill chunk from an empty buffer folds its own records (PFOLD)
+    static_assert(!FOLD || MMA || (NT == 1 && HAS_STATE && WPT == 1 && !TC), "fused fold: decode kind only");
+    constexpr bool PFOLD = FOLD && MMA;
+    constexpr bool DFOLD = FOLD && !MMA;
+    static_assert(!MMA || (HAS_STATE && (WPT == 1 || WPT == 2) && NT >= 2 && !TC),
                   "warp-MMA pass: multi-token state kinds");
     constexpr int NMMA = tc_nmma(NT);
     constexpr int NTHR = TPC * WPT * 32;
@@ -1049,7 +1053,9 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
                     if (obase) obase[t * ostr] = o;
                     const int2 rp = recpos(t);
                     const size_t bh = (size_t)rp.x * Hv + h;
-                    if (!PG || !a.p.btab) ubase[t * kUSub] = us;   // (contiguous records: position j0 + t of slot r)
+                    if constexpr (PFOLD) {
+                        // (folded in this kernel: the delta value is not buffered)
+                    } else if (!PG || !a.p.btab) ubase[t * kUSub] = us;   // (contiguous records: position j0 + t of slot r)
                     else static_cast<UT *>(a.p.U)[((bh * (kD / kUSub) + tile) * dm.bt + rp.y) * kUSub + row] = us;
                     if (dm.keep_raw) {
                         static_cast<InT *>(a.p.V)[(bh * dm.bt + rp.y) * kD + drow] = v_s[t * TPC * 32 + wt * 32 + row];
@@ -1058,7 +1064,7 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
                 }
             }
         }
-        if constexpr (FOLD) {
+        if constexpr (DFOLD) {
             if (J == dm.C) {   // CTA-uniform
                 // S_new = e^{G_t} S0 + U~ K,  U~[row][i] = e^{G_t-G_i} u_i[row] on the
                 // warp-level tensor cores: per warp D[32 rows x 128] = U~ [32 x J] . K [J x 128]
@@ -1135,8 +1141,99 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
                 }
             }
         }
+        if constexpr (PFOLD) {
+            {   // a prefill chunk from an empty buffer (j0 == 0)
+                // S_new = e^{G_last} S0 + sum_t e^{G_last - G_t} u_t k_t^T for the
+                // chunk's n_new records, in the swizzled state tile, per warp
+                // D[32 rows x 128] = Y [32 x n_new] . K [n_new x 128] on mma.sync tf32
+                // (Y = e^{G_last - G_t} u_t split hi + lo; bf16 keys exact, fp32 keys
+                // hi + lo); the record index inside each 8-token k-step is permuted
+                // (slot t <-> token 2t, slot t + 4 <-> 2t + 1) so a B fragment is the
+                // key pair of two consecutive tokens; the A fragments are gathered
+                // from the rows' lanes by shuffles
+                const int g = lane >> 2, t4 = lane & 3;
+                const float gl = Gn_s[n_new - 1], eGl = expf(gl);
+                constexpr int KSN = (NT + 7) / 8;
+                float yv[NT];
+#pragma unroll
+                for (int t = 0; t < NT; ++t) yv[t] = t < n_new ? expf(gl - Gn_s[t]) * un[t] : 0.f;
+                uint32_t yh[KSN][2][4], yl[KSN][2][4];
+#pragma unroll
+                for (int ks = 0; ks < KSN; ++ks)
+#pragma unroll
+                    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            // a_q = Y[row mt*16 + g + 8 (q & 1)][token ks*8 + 2 t4 + (q >> 1)]
+                            const int src = mt * 16 + g + 8 * (q & 1), e = q >> 1;
+                            float v = 0.f;
+#pragma unroll
+                            for (int tt = 0; tt < 4; ++tt) {
+                                const int t = ks * 8 + 2 * tt + e;
+                                const float x = __shfl_sync(0xffffffffu, t < NT ? yv[t < NT ? t : 0] : 0.f, src);
+                                if (tt == t4) v = x;
+                            }
+                            const uint32_t hi = __float_as_uint(v) & 0xFFFFE000u;
+                            yh[ks][mt][q] = hi;
+                            yl[ks][mt][q] = __float_as_uint(v - __uint_as_float(hi));
+                        }
+                auto kval = [&](int t, int c) -> float { return t < n_new ? to_f(k_s[(size_t)t * TS + c]) : 0.f; };
+#pragma unroll 1
+                for (int ng = 0; ng < kD / 32; ++ng) {
+                    float acc[2][4][4] = {};
+#pragma unroll
+                    for (int ks = 0; ks < KSN; ++ks) {
+#pragma unroll
+                        for (int nt = 0; nt < 4; ++nt) {
+                            const int c = ng * 32 + nt * 8 + g;
+                            const float b0 = kval(ks * 8 + 2 * t4, c), b1 = kval(ks * 8 + 2 * t4 + 1, c);
+                            const uint32_t h0 = __float_as_uint(b0) & 0xFFFFE000u, h1 = __float_as_uint(b1) & 0xFFFFE000u;
+#pragma unroll
+                            for (int mt = 0; mt < 2; ++mt) {
+                                mma_tf32_16x8x8(acc[mt][nt], yh[ks][mt], h0, h1);
+                                mma_tf32_16x8x8(acc[mt][nt], yl[ks][mt], h0, h1);
+                                if constexpr (isz == 4)   // fp32 keys: + Y_hi . K_lo
+                                    mma_tf32_16x8x8(acc[mt][nt], yh[ks][mt], __float_as_uint(b0 - __uint_as_float(h0)),
+                                                    __float_as_uint(b1 - __uint_as_float(h1)));
+                            }
+                        }
+                    }
+                    // S = e^{G_last} S + D at rows R = wt*32 + mt*16 + g (+8), columns c, c + 1
+                    unsigned char *Sb = const_cast<unsigned char *>(S_base);
+#pragma unroll
+                    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+                        for (int nt = 0; nt < 4; ++nt) {
+                            const int c = ng * 32 + nt * 8 + 2 * t4;
+#pragma unroll
+                            for (int rh = 0; rh < 2; ++rh) {
+                                const int R = wt * 32 + mt * 16 + g + 8 * rh;
+                                float2 *p = reinterpret_cast<float2 *>(
+                                    Sb + (c >> 5) * (TPC * 4096) + R * 128 + ((((c & 31) >> 2) ^ (R & 7)) << 4) + (c & 3) * 4);
+                                const float2 sv = *p;
+                                *p = make_float2(fmaf(eGl, sv.x, acc[mt][nt][2 * rh]), fmaf(eGl, sv.y, acc[mt][nt][2 * rh + 1]));
+                            }
+                        }
+                }
+            }
+        }
     }
-    if constexpr (FOLD) {
+    if constexpr (PFOLD) {
+        {   // the CTA's folded rows leave as TMA box stores
+            fence_proxy_async_smem();
+            __syncthreads();
+            if (tid == 0) {
+                const int row0 = (int)((sb * Hv + h) * kD) + tile0 * 32;
+#pragma unroll
+                for (int kb = 0; kb < 4; ++kb)
+#pragma unroll
+                    for (int x = 0; x < TPC; ++x)
+                        tma_store_2d(&tmap, S_base + kb * (TPC * 4096) + x * 4096, kb * 32, row0 + x * 32);
+                bulk_commit();
+            }
+        }
+    }
+    if constexpr (DFOLD) {
         if (J == dm.C) {   // CTA-uniform: one bulk store of the CTA's folded rows
             fence_proxy_async_smem();
             __syncthreads();
@@ -1177,12 +1274,15 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
     if (a.kind != CK_VERIFY && tid == 0 && ticket == (int)(gridDim.x * gridDim.y) - 1) {
         a.p.ticket[r] = 0;
         if (direct) a.p.len[r] = J;
-        else a.p.occ[r] = (FOLD && J == dm.C) ? 0 : J;
+        else a.p.occ[r] = ((DFOLD && J == dm.C) || PFOLD) ? 0 : J;
     }
     if (bad) atomicOr(a.p.status, bad);
     CK_MARK(3);
-    if constexpr (FOLD) {
+    if constexpr (DFOLD) {
         if (J == dm.C && tid == 0) bulk_wait_read0();   // shared memory stays live until the store has read it
+    }
+    if constexpr (PFOLD) {
+        if (tid == 0) bulk_wait_read0();
     }
 }
 
@@ -1196,8 +1296,8 @@ static cudaError_t launch_cfg(const ChunkArgs &a, cudaStream_t s) {
     if (a.n > kMaxSlotsPerLaunch) return cudaErrorInvalidConfiguration;
     // pools / index lists: the PG instantiation (not for the TC or fused-fold kinds)
     const bool pg = a.slots || a.pos || a.p.btab || a.p.sidx;
-    if (pg && (TC || FOLD)) return cudaErrorInvalidValue;
-    auto kfn = pg ? chunk_cta_kernel<InT, UT, TPC, WPT, NT, HAS_STATE, MINB < 1 ? 1 : MINB, TC && !TC, FOLD && !FOLD, MMA, true>
+    if (pg && (TC || (FOLD && !MMA))) return cudaErrorInvalidValue;
+    auto kfn = pg ? chunk_cta_kernel<InT, UT, TPC, WPT, NT, HAS_STATE, MINB < 1 ? 1 : MINB, TC && !TC, FOLD && MMA, MMA, true>
                   : chunk_cta_kernel<InT, UT, TPC, WPT, NT, HAS_STATE, MINB < 1 ? 1 : MINB, TC, FOLD, MMA, false>;
     cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.bytes);
     if (e != cudaSuccess) return e;
@@ -1216,6 +1316,14 @@ static cudaError_t launch_cfg(const ChunkArgs &a, cudaStream_t s) {
 template <typename InT, typename UT, int TPC, int WPT, bool HAS_STATE, int MBO = 0, bool TC = false, bool MMA = false>
 static cudaError_t launch_nt(const ChunkArgs &a, cudaStream_t s) {
     if (!TC && !MMA && a.n_new == 1) return launch_cfg<InT, UT, TPC, WPT, 1, HAS_STATE, MBO, TC>(a, s);
+    if constexpr (MMA) {   // (prefill chunk that folds its own records)
+        if (a.pfold) {
+            if (a.n_new <= 2) return launch_cfg<InT, UT, TPC, WPT, 2, HAS_STATE, MBO, TC, true, MMA>(a, s);
+            if (a.n_new <= 4) return launch_cfg<InT, UT, TPC, WPT, 4, HAS_STATE, MBO, TC, true, MMA>(a, s);
+            if (a.n_new <= 8) return launch_cfg<InT, UT, TPC, WPT, 8, HAS_STATE, MBO, TC, true, MMA>(a, s);
+            return launch_cfg<InT, UT, TPC, WPT, 16, HAS_STATE, MBO, TC, true, MMA>(a, s);
+        }
+    }
     if (a.n_new <= 2) return launch_cfg<InT, UT, TPC, WPT, 2, HAS_STATE, MBO, TC, false, MMA>(a, s);
     if (a.n_new <= 4) return launch_cfg<InT, UT, TPC, WPT, 4, HAS_STATE, MBO, TC, false, MMA>(a, s);
     if (a.n_new <= 8) return launch_cfg<InT, UT, TPC, WPT, 8, HAS_STATE, MBO, TC, false, MMA>(a, s);

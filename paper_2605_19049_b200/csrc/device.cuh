@@ -229,6 +229,11 @@ __device__ __forceinline__ void tma_load_2d(void *dst_smem, const void *tmap, in
         "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
         ::"r"(smem_u32(dst_smem)), "l"(tmap), "r"(c0), "r"(c1), "r"(smem_u32(bar)) : "memory");
 }
+// 2-D TMA tile store (shared -> global, bulk-group completion).
+__device__ __forceinline__ void tma_store_2d(const void *tmap, const void *src_smem, int c0, int c1) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];"
+                 ::"l"(tmap), "r"(smem_u32(src_smem)), "r"(c0), "r"(c1) : "memory");
+}
 // UMMA descriptor, K-major SWIZZLE_128B (the layout a 128-byte-wide TMA box
 // with CU_TENSOR_MAP_SWIZZLE_128B writes): 8-row x 128-byte atoms, 1024 B
 // apart; K steps inside an atom advance the start address.

@@ -82,10 +82,6 @@ __host__ __device__ inline UtSmem ut_smem_layout() {
 __device__ __forceinline__ uint32_t ut_sw(int j, int c) {
     return (uint32_t)((c >> 5) * 16384 + j * 128 + ((((c & 31) >> 2) ^ (j & 7)) << 4) + (c & 3) * 4);
 }
-__device__ __forceinline__ void tma_store_2d(const void *tmap, const void *src_smem, int c0, int c1) {
-    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];"
-                 ::"l"(tmap), "r"(smem_u32(src_smem)), "r"(c0), "r"(c1) : "memory");
-}
 __device__ __forceinline__ void split_tf32(uint32_t x, uint32_t &hi, uint32_t &lo) {
     hi = x & 0xFFFFE000u;
     lo = __float_as_uint(__uint_as_float(x) - __uint_as_float(hi));

@@ -93,6 +93,8 @@ struct ChunkArgs {
     int dry = 0;        // 1: check the launch configuration only, enqueue nothing
     int pdl = 0, pdl_early = 0;   // see Ptrs/launch overlap below
     int fold = 0;                 // decode: fold a slot's buffer in the step that fills it
+    int pfold = 0;                // prefill chunk from an empty buffer (warp-MMA kinds): fold the chunk's
+                                  // records into the state tile in the same kernel (no records written)
     const void *tmapk = nullptr;  // direct one-token step: host CUtensorMap of the bf16 key records as
                                   // [R*Hk*T][128] (16 x 64 boxes, 128 B swizzle) -- key rows on the tensor cores
     const void *tmap = nullptr;   // host CUtensorMap of the state as [R*Hv*128][128] fp32

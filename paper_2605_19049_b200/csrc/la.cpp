@@ -302,7 +302,7 @@ cudaError_t run_chunk(la_buf *b, int first, int n, int n_tok, int j0_cap, int to
                       int kind, const void *q, const void *k, const void *v, const float *alpha,
                       const float *beta, float *o, cudaStream_t s, int fold = 0,
                       const int *slots = nullptr, const int *pos = nullptr, int passes = 3, int seg = 0,
-                      bool j0_uniform = false) {
+                      bool j0_uniform = false, int pfold = 0) {
     const int mx = max_new_per_launch(b->dm.g);
     const size_t isz = dt_size(b->cfg.in_dtype);
     const size_t d = kD;
@@ -334,13 +334,14 @@ cudaError_t run_chunk(la_buf *b, int first, int n, int n_tok, int j0_cap, int to
                 a.tmap = (kind == CK_VERIFY || kind == CK_PREFILL) && m >= 2 ? state_tmap(b) : nullptr;
                 a.tmapk = (kind == CK_DIRECT && m == 1 && !slots) ? key_tmap(b) : nullptr;
                 a.fold = fold;
+                a.pfold = (pfold && m >= 2 && a.tmap) ? 1 : 0;
                 a.seg = seg;
                 a.dry = pass == 0;
                 overlap_flags(b, s, a);
                 if (slots) a.pdl_early = 0;   // the slot list itself comes from a previous grid
                 cudaError_t e = launch_chunk(a, s, &b->launches);
                 if (e != cudaSuccess) return e;
-                if (pass == 1) note_launch(b, s, fold != 0);
+                if (pass == 1) note_launch(b, s, fold != 0 || a.pfold != 0);   // (a folding launch writes the state)
             }
         }
     }
@@ -953,8 +954,14 @@ la_status la_prefill(la_buf *b, int32_t first, int32_t n, int32_t n_tok, const v
     }
     for (int c0 = 0; c0 < n_tok; c0 += C) {
         const int cn = std::min(C, n_tok - c0);
-        cudaError_t e = run_chunk(b, first, n, cn, 0, c0, n_tok, CK_PREFILL, q, k, v, alpha, beta, o, s);
+        // a chunk of 2..16 tokens is one warp-MMA launch that also folds its
+        // records into the state (the buffer is empty at every chunk start):
+        // one state read and one write per chunk instead of two reads
+        const bool pf = cn >= 2 && cn <= max_new_per_launch(b->dm.g) && state_tmap(b) != nullptr;
+        cudaError_t e = run_chunk(b, first, n, cn, 0, c0, n_tok, CK_PREFILL, q, k, v, alpha, beta, o, s, 0, nullptr,
+                                  nullptr, 3, 0, false, pf ? 1 : 0);
         if (e != cudaSuccess) return cuda_fail(e, "prefill chunk launch (the handle's slots are undefined: reset them)");
+        if (pf) continue;
         FoldArgs f;
         f.dm = b->dm; f.p = b->p; f.first = first; f.n = n; f.kind = FK_FORCE; f.nacc = nullptr; f.n_draft = 0;
         f.kcap = cn; f.spec = 1;
