@@ -1005,8 +1005,13 @@ def row_prefill(torch, L, cost, sd, dev, stream, seed, peak, B=64, n_tok=1024):
         _, (ms,) = timed_graphs(torch, stream, [g], 5, 3)
         ms /= 5
         # per chunk: launches of 16 tokens (state + inputs + the chunk's earlier
-        # records read, outputs + records written) + the fold of the chunk
-        per_chunk = sum(lb.st + 16 * (lb.inp + lb.o + lb.rec) + 16 * j * lb.rec for j in range(PC // 16)) + lb.flush(PC)
+        # records read, outputs + records written) + the fold of the chunk;
+        # a chunk of <= 16 tokens is one launch that folds its own records
+        # (state read + state written + inputs + outputs, no records)
+        if PC <= 16:
+            per_chunk = 2 * lb.st + PC * (lb.inp + lb.o)
+        else:
+            per_chunk = sum(lb.st + 16 * (lb.inp + lb.o + lb.rec) + 16 * j * lb.rec for j in range(PC // 16)) + lb.flush(PC)
         nbytes = B * per_chunk * (n_tok // PC)
         res[PC] = {"ms": ms, "tokens_per_s": B * n_tok / (ms * 1e-3), "algorithmic_bytes": nbytes,
                    "gbs": nbytes / (ms * 1e-3) / 1e9, "frac_of_measured": nbytes / (ms * 1e-3) / (peak * 1e9),
