@@ -1357,7 +1357,7 @@ cudaError_t launch_state(const ChunkArgs &a, cudaStream_t s) {
     // the CUDA-core pass is the fallback without a tensor map
     // (8 or more tokens: the whole head per CTA -- the key rows are computed
     // once per head; measured verify N = 8 162 -> 150 us, N = 4 109 -> 123)
-    if (a.n_new >= 8 && a.tmap) return launch_nt<InT, UT, 4, kMmaWPT, true, 0, false, true>(a, s);
+    if (a.n_new >= 8 && a.tmap && !a.pfold) return launch_nt<InT, UT, 4, kMmaWPT, true, 0, false, true>(a, s);
     if (a.n_new >= 2 && a.tmap) return launch_nt<InT, UT, kChunkTPC, kMmaWPT, true, 0, false, true>(a, s);
     return launch_nt<InT, UT, kChunkTPC, 1, true>(a, s);
 }
