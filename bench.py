@@ -583,6 +583,9 @@ def main(argv=None):
                              "events around the captured decode graph; traffic = ncu dram bytes per launch "
                              "(profiles/ncu_traffic.json)"},
         "gpu_launches": launches_per_step * K,
+        # environment overrides that change what runs (the library path; the
+        # NCCL path of the TP helpers): recorded, never silent
+        "env_overrides": {k: os.environ[k] for k in ("LABUF_LIB", "LABUF_NCCL_LIB") if k in os.environ},
     }
 
     # ---- e2e through the public API with host buffers: every step copies
