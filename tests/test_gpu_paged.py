@@ -203,3 +203,41 @@ def test_block_and_state_ids_are_deterministic(cuda_device):
         buf.reset(5, 1, mode=L.LA_MODE_CHUNKWISE)
         ids.append([buf.pool_info(r)["slot_state"] for r in range(6)])
     assert ids[0] == ids[1] == [-1, 0, -1, -1, 2, 1]
+
+
+@pytest.mark.parametrize("in_dtype,bt", [("bf16", 16), ("f32", 8)])
+def test_paged_prefill_self_fold(cuda_device, in_dtype, bt):
+    """Prefill on a paged handle with a state pool whose slot -> state map is
+    not the identity: 16-token chunks fold their own records into the pooled
+    state (TMA stores through the state index) and a ragged tail; outputs,
+    states and the next decode step vs the oracle."""
+    rc = synth.Recipe(seed=3150 + bt, dist="stress", in_dtype=in_dtype)
+    tol = TOL[in_dtype]
+    R, C, n_tok = 4, 16, 77
+    buf = _paged(R, C, bt=bt, in_dtype=in_dtype, states=R + 2)
+    # states handed out in reverse slot order: slot r -> state R - 1 - r (+ the spares stay free)
+    for r in reversed(range(R)):
+        buf.reset(r, 1, zero_state=False)
+    assert [buf.pool_info(r)["slot_state"] for r in range(R)] == list(reversed(range(R)))
+    allslots = np.arange(R)
+    S0 = synth.state0(rc, allslots, HV, 128, 128)
+    set_states(buf, S0, allslots)
+    orc = Oracle(S0)
+    slots = np.arange(1, R)                       # a range that does not start at slot 0
+    tok = synth.tokens(rc, slots, np.arange(n_tok), HK, HV, 128)
+    ref = orc.run(slots, tok)
+    d = upload_tokens(tok, in_dtype, cuda_device)
+    o = torch.empty(len(slots), n_tok, HV, 128, dtype=torch.float32, device=cuda_device)
+    buf.prefill(1, d["q"], d["k"], d["v"], d["alpha"], d["beta"], o)
+    assert_close(o.cpu().numpy(), ref, tol, "paged prefill outputs")
+    for s in allslots:   # (slot 0 untouched)
+        assert_close(buf.state_get(int(s)).cpu().numpy(), orc.S[s], tol, f"paged prefill state, slot {s}")
+    nxt = synth.tokens(rc, slots, [n_tok], HK, HV, 128)
+    r1 = orc.run(slots, nxt)
+    d1 = upload_tokens(nxt, in_dtype, cuda_device, squeeze_t=True)
+    o1 = torch.empty(len(slots), HV, 128, dtype=torch.float32, device=cuda_device)
+    buf.decode_step(1, d1["q"], d1["k"], d1["v"], d1["alpha"], d1["beta"], o1)
+    assert_close(o1.cpu().numpy(), r1[:, 0], tol, "decode after paged prefill")
+    _invariants(buf, R)
+    flags, (occ, _, _) = buf.device_status()
+    assert flags == 0 and occ[1:] == [1] * (R - 1)
