@@ -99,8 +99,13 @@ __host__ __device__ inline CtaLayout cta_layout(int TPC, int nt, bool has_state,
     L.Ck = o; o = al128(o + (uint32_t)(ntp(nt) * J * 4));
     L.Cq = o; o = al128(o + (uint32_t)(ntp(nt) * J * 4));
     // (the MMA kinds keep S0 k_t, S0 q_t in registers and shuffle them to the rows)
-    L.av = o; o = al128(o + (uint32_t)(has_state && !mma ? TPC * nt * 32 * 4 : 0));
-    L.bv = o; o = al128(o + (uint32_t)(has_state && !mma ? TPC * nt * 32 * 4 : 0));
+    // (self-folding prefill chunks of 8+ tokens stash S0 k_t, S0 q_t here once
+    //  instead of shuffling them to the substitution lanes per token; measured:
+    //  prefill 7.55 -> 7.39 ms, but verify N = 8 149.5 -> 201.6 us from the
+    //  extra shared memory, so not for verify)
+    const bool stash_ = has_state && mma && fold && nt >= 8;
+    L.av = o; o = al128(o + (uint32_t)(has_state && (!mma || stash_) ? TPC * nt * 32 * 4 : 0));
+    L.bv = o; o = al128(o + (uint32_t)(has_state && (!mma || stash_) ? TPC * nt * 32 * 4 : 0));
     L.Gn = o; o = al128(o + (uint32_t)(nt * 4));
     L.Bn = o; o = al128(o + (uint32_t)(nt * 4));
     L.Y = o;  o = al128(o + (tc ? (uint32_t)(tc_nmma(nt) * kD * 4 * (isz == 4 ? 2 : 1)) : 0u));
@@ -885,6 +890,19 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
         }
         // D[row][2 t + {0, 1}] = (S0 k_t, S0 q_t) of token t = 4 j + t4: stays in
         // registers; the substitution shuffles each row's values to its lane
+        // (8+ tokens: stashed per (token, row) instead -- 2 loads per token)
+        if constexpr (NT >= 8 && FOLD) {
+            const int g = lane >> 2, t4 = lane & 3;
+#pragma unroll
+            for (int mt = 0; mt < MTW; ++mt)
+#pragma unroll
+                for (int j = 0; j < NJ; ++j)
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const int t = 4 * j + t4, rr = (half * MTW + mt) * 16 + g + 8 * (q >> 1);
+                        if (t < NT) ((q & 1) ? bv : av)[(wt * NT + t) * 32 + rr] = acc[mt][j][q];
+                    }
+        }
     }
     if constexpr (TC) {
         // pass 2 on the exact remainder S0 - trunc(S0), written in place once
@@ -1020,7 +1038,10 @@ __global__ void __launch_bounds__(TPC * WPT * 32, MINB) chunk_cta_kernel(const C
                 const float bt = Bn_s[t];
                 const float eG = __shfl_sync(0xffffffffu, eg_l, t);
                 float u, o;
-                if constexpr (MMA) {
+                if constexpr (MMA && NT >= 8 && FOLD) {
+                    u = bt * (vt - fmaf(eG, av[(wt * NT + t) * 32 + row], acc_k));
+                    o = fmaf(eG, bv[(wt * NT + t) * 32 + row], acc_q);
+                } else if constexpr (MMA) {
                     // (S0 k_t, S0 q_t) of this row from the fragment holder: lane
                     // 4 (row % 8) + t % 4 holds rows g, g + 8 of each m-tile
                     static_assert(!MMA || WPT == 1, "row = lane");
