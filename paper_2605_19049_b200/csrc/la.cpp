@@ -1100,11 +1100,30 @@ la_status la_decode_mixed(la_buf *b, int32_t n, const int32_t *slots, const void
     // launch configurations first (all-or-nothing)
     const int *W_CW = wl_ptr(b, WL_CW), *W_CWP = wl_ptr(b, WL_CW_POS), *W_DR = wl_ptr(b, WL_DR),
               *W_DRP = wl_ptr(b, WL_DR_POS), *W_FL = wl_ptr(b, WL_FL), *W_CP = wl_ptr(b, WL_CP);
+    // a group whose slots and input rows are both consecutive launches as a
+    // plain range (no work-list loads in front of every CTA's state request):
+    // the slots' own range and the inputs offset to its first row
+    auto consecutive = [](const std::vector<int> &x) {
+        for (size_t i = 1; i < x.size(); ++i)
+            if (x[i] != x[0] + (int)i) return false;
+        return !x.empty();
+    };
+    const size_t isz = dt_size(b->cfg.in_dtype), dd = kD;
+    const int Hk = b->dm.Hk, Hv = b->dm.Hv;
+    auto launch_group = [&](const std::vector<int> &sl, const std::vector<int> &pos, int j0c, int kind,
+                            const int *W, const int *WP, int passes) -> cudaError_t {
+        if (consecutive(sl) && consecutive(pos)) {
+            const size_t p0 = (size_t)pos[0];
+            return run_chunk(b, sl[0], (int)sl.size(), 1, j0c, 0, 1, kind,
+                             static_cast<const char *>(q) + p0 * Hk * dd * isz, static_cast<const char *>(k) + p0 * Hk * dd * isz,
+                             static_cast<const char *>(v) + p0 * Hv * dd * isz, alpha + p0 * Hv, beta + p0 * Hv,
+                             o ? o + p0 * Hv * dd : nullptr, s, 0, nullptr, nullptr, passes);
+        }
+        return run_chunk(b, 0, (int)sl.size(), 1, j0c, 0, 1, kind, q, k, v, alpha, beta, o, s, 0, W, WP, passes);
+    };
     cudaError_t e = cudaSuccess;
-    if (!cw.empty())
-        e = run_chunk(b, 0, (int)cw.size(), 1, j0_cw, 0, 1, CK_DECODE, q, k, v, alpha, beta, o, s, 0, W_CW, W_CWP, 1);
-    if (e == cudaSuccess && !dr.empty())
-        e = run_chunk(b, 0, (int)dr.size(), 1, j0_dr, 0, 1, CK_DIRECT, q, k, v, alpha, beta, o, s, 0, W_DR, W_DRP, 1);
+    if (!cw.empty()) e = launch_group(cw, cw_pos, j0_cw, CK_DECODE, W_CW, W_CWP, 1);
+    if (e == cudaSuccess && !dr.empty()) e = launch_group(dr, dr_pos, j0_dr, CK_DIRECT, W_DR, W_DRP, 1);
     if (e != cudaSuccess) return cuda_fail(e, "mixed decode launch configuration");
     // pools and work lists -> one staging pass
     Stage stg;
@@ -1126,17 +1145,14 @@ la_status la_decode_mixed(la_buf *b, int32_t n, const int32_t *slots, const void
         a.kind = FK_FORCE; a.nacc = nullptr; a.n_draft = 0; a.kcap = cp_cap; a.spec = 0;
         if ((e = run_fold(b, a, s)) != cudaSuccess) return cuda_fail(e, "compression launch");
     }
-    if (!cw.empty() &&
-        (e = run_chunk(b, 0, (int)cw.size(), 1, j0_cw, 0, 1, CK_DECODE, q, k, v, alpha, beta, o, s, 0, W_CW, W_CWP,
-                       2)) != cudaSuccess)
+    if (!cw.empty() && (e = launch_group(cw, cw_pos, j0_cw, CK_DECODE, W_CW, W_CWP, 2)) != cudaSuccess)
         return cuda_fail(e, "mixed decode launch");
-    if (!dr.empty() &&
-        (e = run_chunk(b, 0, (int)dr.size(), 1, j0_dr, 0, 1, CK_DIRECT, q, k, v, alpha, beta, o, s, 0, W_DR, W_DRP,
-                       2)) != cudaSuccess)
+    if (!dr.empty() && (e = launch_group(dr, dr_pos, j0_dr, CK_DIRECT, W_DR, W_DRP, 2)) != cudaSuccess)
         return cuda_fail(e, "mixed direct launch");
     if (!fl.empty()) {   // eager flush of the buffers this step filled (Z15)
         FoldArgs a;
         a.dm = b->dm; a.p = b->p; a.first = 0; a.n = (int)fl.size(); a.slots = W_FL;
+        if (consecutive(fl)) { a.first = fl[0]; a.slots = nullptr; }
         a.kind = FK_FULL; a.nacc = nullptr; a.n_draft = 0; a.kcap = C; a.spec = 1;
         if ((e = run_fold(b, a, s)) != cudaSuccess) return cuda_fail(e, "flush launch");
     }
