@@ -6,12 +6,12 @@ TAG=${1:-sweep_c2}
 OUT=gpurun_out/$TAG
 mkdir -p $OUT
 run() {  # batch chunk layers
-  timeout 600 python bench.py --no-rows --no-cpu --no-e2e --steps 10 --warmup 3 \
+  timeout 600 python bench.py --no-rows --no-cpu --no-e2e --no-config1 --no-config5 --steps 10 --warmup 3 \
       --batch $1 --chunk $2 --layers $3 > $OUT/b_$1_$2.json 2> $OUT/b_$1_$2.err
   python - $OUT/b_$1_$2.json $1 $2 <<'PY' >> $OUT/summary.txt
 import json, sys
 try:
-    d = json.load(open(sys.argv[1]))
+    d = json.loads(open(sys.argv[1]).read().strip().splitlines()[-1])
     k = d["kernels"]
     row = {"batch": int(sys.argv[2]), "chunk": int(sys.argv[3]), "us_per_token": d["us_per_token"],
            "recurrent_us_per_token": d["recurrent"]["us_per_token"], "speedup": d["speedup_vs_recurrent"],
