@@ -22,6 +22,8 @@
 // the row-major state tile), adds e^{G_last} S0 in shared memory and one
 // bulk store writes S_new back.  Shared memory is sized from the host-known
 // largest record count, so 4 CTAs share an SM at C = 16.
+#include <cstdlib>
+
 #include "device.cuh"
 #include "internal.h"
 
@@ -51,6 +53,56 @@ __host__ __device__ inline FoldSmem fold_smem_layout(bool fp32_in, int nj, int k
 // at +kc*32 B (SBO).
 __device__ __forceinline__ uint32_t kmaj_off(int row, int k, int kc) {
     return (uint32_t)((row >> 3) * (kc * 32) + (k >> 2) * 128 + (row & 7) * 16 + (k & 3) * 4);
+}
+
+// Which records a fold launch folds for slot r (uniform over the slot's
+// CTAs): meta[0] = n, meta[1] = S0 is zero (compression), meta[2..3] = the
+// branch remap (FK_BRANCH: record i >= meta[2] is record i + meta[3]),
+// meta[4] = the last folded record's log decay G_last.
+__device__ __forceinline__ size_t recb_h(int2 ba, int Hv, int h, int bt) { return ((size_t)ba.x * Hv + h) * bt + ba.y; }
+
+template <bool PG>
+__device__ __forceinline__ void fold_counters(const FoldArgs &a, int r, int zi, int h, int *meta) {
+    const Dims &dm = a.dm;
+    const int mode = a.p.mode[r], occ = a.p.occ[r], len = a.p.len[r];
+    int n = 0;
+    bool zero_s0 = false;
+    meta[2] = 1 << 30;
+    meta[3] = 0;
+    if (a.kind == FK_FULL) {
+        n = (mode == 0 && occ == dm.C) ? occ : 0;
+    } else if (a.kind == FK_FORCE) {
+        if (mode == 1) { n = len; zero_s0 = true; } else n = occ;
+    } else if (a.kind == FK_FORK) {
+        n = a.fork_n;
+        zero_s0 = mode == 1;
+    } else if (a.kind == FK_BRANCH) {
+        int na = a.nacc[zi], br = a.branch[zi];
+        if (na < 0 || na > a.n_draft || br < 0 || br >= a.n_branch) {
+            if (dm.validate) atomicOr(a.p.status, 0x8u);
+            na = na < 0 ? 0 : (na > a.n_draft ? a.n_draft : na);
+            br = br < 0 ? 0 : (br >= a.n_branch ? a.n_branch - 1 : br);
+        }
+        n = occ + na;
+        meta[2] = occ;
+        meta[3] = br * a.n_draft;
+    } else {  // FK_COMMIT
+        int na = a.nacc[zi];
+        if (na < 0 || na > a.n_draft) {
+            if (dm.validate) atomicOr(a.p.status, 0x8u);
+            na = na < 0 ? 0 : a.n_draft;
+        }
+        n = occ + na;
+    }
+    meta[0] = n;
+    meta[1] = zero_s0;
+    // the last folded record's log decay, read here with the counters (off
+    // the post-barrier critical path); branch commits remap past occ
+    if (n > 0) {
+        const int last = (a.kind == FK_BRANCH && n - 1 >= occ) ? n - 1 + meta[3] : n - 1;
+        const int2 ba = PG ? rec_at(dm, a.p, r, last) : make_int2(r, last);
+        meta[4] = __float_as_int(a.p.G[((size_t)ba.x * dm.Hv + h) * dm.bt + ba.y]);
+    }
 }
 
 // (Mode ii, the UT transform from the raw records, is fold_ut.cu.)
@@ -146,44 +198,8 @@ __global__ void __launch_bounds__(kFoldThreads, kFoldNJ == 128 ? 2 : (kFoldNJ ==
     pdl_trigger();
     if (tid == 32) {
         if (a.spec && !a.pdl_early) bulk_g2s(S_s, state_tile, kFoldNJ * kD * 4, bar_ld);
-        const int mode = a.p.mode[r], occ = a.p.occ[r], len = a.p.len[r];
-        int n = 0;
-        bool zero_s0 = false;
-        if (a.kind == FK_FULL) {
-            n = (mode == 0 && occ == dm.C) ? occ : 0;
-        } else if (a.kind == FK_FORCE) {
-            if (mode == 1) { n = len; zero_s0 = true; } else n = occ;
-        } else if (a.kind == FK_FORK) {
-            n = a.fork_n;
-            zero_s0 = mode == 1;
-        } else if (a.kind == FK_BRANCH) {
-            int na = a.nacc[zi], br = a.branch[zi];
-            if (na < 0 || na > a.n_draft || br < 0 || br >= a.n_branch) {
-                if (dm.validate) atomicOr(a.p.status, 0x8u);
-                na = na < 0 ? 0 : (na > a.n_draft ? a.n_draft : na);
-                br = br < 0 ? 0 : (br >= a.n_branch ? a.n_branch - 1 : br);
-            }
-            n = occ + na;
-            meta[2] = occ;
-            meta[3] = br * a.n_draft;
-        } else {  // FK_COMMIT
-            int na = a.nacc[zi];
-            if (na < 0 || na > a.n_draft) {
-                if (dm.validate) atomicOr(a.p.status, 0x8u);
-                na = na < 0 ? 0 : a.n_draft;
-            }
-            n = occ + na;
-        }
-        meta[0] = n;
-        meta[1] = zero_s0;
-        // the last folded record's log decay, read here with the counters (off
-        // the post-barrier critical path); branch commits remap past occ
-        if (n > 0) {
-            const int last = (a.kind == FK_BRANCH && n - 1 >= occ) ? n - 1 + meta[3] : n - 1;
-            const int2 ba = PG ? rec_at(dm, a.p, r, last) : make_int2(r, last);
-            meta[4] = __float_as_int(a.p.G[((size_t)ba.x * Hv + h) * bt + ba.y]);
-        }
-        if (!a.spec && n > 0 && !zero_s0) {
+        fold_counters<PG>(a, r, zi, h, meta);
+        if (!a.spec && meta[0] > 0 && !meta[1]) {
             mbar_arrive_expect_tx(bar_ld, kFoldNJ * kD * 4);
             bulk_g2s(S_s, state_tile, kFoldNJ * kD * 4, bar_ld);
         }
@@ -305,6 +321,214 @@ __global__ void __launch_bounds__(kFoldThreads, kFoldNJ == 128 ? 2 : (kFoldNJ ==
     }
 }
 
+// Warp-MMA form of kernel (2): the same fold with the rank-n update on
+// mma.sync (m16n8k8 tf32, fp32 accumulate in registers) and no TMEM.
+// Allocating TMEM costs every CTA ~0.5 us of SM-serialised time
+// (tools/microbench_tmem.cu), ~30 us per SM over a config-2 flush's 8192
+// CTAs; this form drops it.  One 4-warp CTA per (32 d_v rows, V head,
+// slot): the 16 KiB S0 tile streams into shared memory with one bulk copy
+// and the chunk's key rows and u values with cp.async, so the registers hold
+// only the accumulators (8 CTAs per SM, 128 KiB of state in flight per SM).
+// Warp w owns key columns c in [32 w, 32 w + 32).  The MMA rows (M) are key
+// columns and the columns (N) d_v rows, both permuted so that every
+// thread's accumulators are whole float4 rows of the state: M row g / g + 8
+// of m-tile mt is column c0 + 2 mt + 0 / 1 (c0 = 32 w + 4 g), N column n of
+// n-tile nt is d_v row 4 n + nt.  Thread (g, t) then holds S[j][c0 .. c0 +
+// 3] for j = 8 t + 4 p + nt (p, nt in 0..1 x 0..3); the epilogue adds
+// e^{G_last} S0 from shared memory (float4, conflict-free) and stores the
+// rows straight to HBM (128 B per 8 lanes).  fp32 accuracy: split-TF32 as
+// in the tcgen05 form (bf16 keys exact; fp32 keys split too).
+template <typename InT, typename UT, bool FP32_IN, bool PG, int MINB>
+__global__ void __launch_bounds__(kFoldThreads, MINB) fold_wm_kernel(const FoldArgs a) {
+    static_assert(kUSub == 32, "one U sub-tile per CTA");
+    constexpr int KB = kD * (int)sizeof(InT);   // bytes per key row
+    constexpr int UB = 32 * (int)sizeof(UT);    // bytes of u_i per CTA
+    const int jh = blockIdx.x, h = blockIdx.y, zi = blockIdx.z;
+    if constexpr (PG) {
+        if (a.pdl) pdl_wait();
+    }
+    const int r = PG && a.slots ? __ldcg(a.slots + zi) : a.first + zi;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+    const Dims dm = a.dm;
+    const int Hv = dm.Hv, bt = dm.bt, hk = h / dm.g;
+    __shared__ __align__(128) float S_s[32 * kD];
+    __shared__ __align__(128) unsigned char K_s[16 * KB];
+    __shared__ __align__(128) unsigned char U_s[16 * UB];
+    __shared__ uint64_t bar_ld;
+    __shared__ int meta[5];
+    const size_t sb = PG && a.p.sidx ? (size_t)__ldcg(a.p.sidx + r) : (size_t)r;
+    const float *state_tile = a.p.state + ((sb * Hv + h) * kD + (size_t)jh * 32) * kD;
+    float *state_out = const_cast<float *>(state_tile);
+    if (a.kind == FK_FORK) {
+        const size_t db = PG && a.p.sidx ? (size_t)__ldcg(a.p.sidx + a.fork_dst) : (size_t)a.fork_dst;
+        state_out = a.p.state + ((db * Hv + h) * kD + (size_t)jh * 32) * kD;
+    }
+    const int c0 = warp * 32 + 4 * g;
+
+    int bocc = 1 << 30, boff = 0;
+    auto at = [&](int i) -> int2 {
+        const int ii = i >= bocc ? i + boff : i;
+        return PG ? rec_at(dm, a.p, r, ii) : make_int2(r, ii);
+    };
+    // chunk kc0 .. kc0 + kn - 1: key rows and u values into shared memory
+    // (cp.async), this thread's log decays G for tokens t + 4 s into gv
+    float gv[4];
+    auto load_chunk = [&](int kc0, int kn) {
+        const int2 b0 = at(kc0);
+        const int lim = (kc0 < bocc && kc0 + 16 > bocc) ? 0 : ((PG && a.p.btab) ? bt - b0.y : (1 << 30));
+        auto ba_of = [&](int i) -> int2 { return i < lim ? make_int2(b0.x, b0.y + i) : at(kc0 + i); };
+#pragma unroll
+        for (int q = 0; q < 16 * KB / 16 / kFoldThreads; ++q) {
+            const int idx = q * kFoldThreads + tid, i = idx / (KB / 16), seg = idx % (KB / 16);
+            if (i < kn) {
+                const int2 ba = ba_of(i);
+                cp_async16(K_s + i * KB + seg * 16,
+                           reinterpret_cast<const unsigned char *>(a.p.K) +
+                               ((((size_t)ba.x * dm.Hk + hk) * bt + ba.y) * kD) * sizeof(InT) + seg * 16);
+            }
+        }
+        if (tid < 16 * UB / 16) {
+            const int i = tid / (UB / 16), seg = tid % (UB / 16);
+            if (i < kn) {
+                const int2 ba = ba_of(i);
+                cp_async16(U_s + i * UB + seg * 16,
+                           reinterpret_cast<const unsigned char *>(a.p.U) +
+                               (((((size_t)ba.x * Hv + h) * (kD / kUSub) + jh) * bt + ba.y) * kUSub) * sizeof(UT) + seg * 16);
+            }
+        }
+        cp_async_commit();
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {
+            const int i = t + 4 * s;
+            gv[s] = i < kn ? a.p.G[recb_h(ba_of(i), Hv, h, bt)] : 0.f;
+        }
+    };
+
+    if (tid == 32) {
+        mbar_init(&bar_ld, 1);
+        fence_mbar_init();
+        if (a.spec) {
+            mbar_arrive_expect_tx(&bar_ld, 32 * kD * 4);
+            if (a.pdl_early) bulk_g2s(S_s, state_tile, 32 * kD * 4, &bar_ld);
+        }
+    }
+    if (a.pdl) pdl_wait();   // counters, records (and the state unless pdl_early) may come from the previous grid
+    pdl_trigger();
+    if (tid == 32) {
+        if (a.spec && !a.pdl_early) bulk_g2s(S_s, state_tile, 32 * kD * 4, &bar_ld);
+        fold_counters<PG>(a, r, zi, h, meta);
+        if (!a.spec && meta[0] > 0 && !meta[1]) {
+            mbar_arrive_expect_tx(&bar_ld, 32 * kD * 4);
+            bulk_g2s(S_s, state_tile, 32 * kD * 4, &bar_ld);
+        }
+    }
+    if (a.kind != FK_BRANCH) load_chunk(0, min(16, a.kcap));
+    __syncthreads();
+    const int n = meta[0];
+    const bool zero_s0 = meta[1] != 0;
+    if (n == 0) {   // nothing to fold: state untouched, counters unchanged
+        cp_async_wait_all();
+        if (a.spec) mbar_wait(&bar_ld, 0);   // the speculative copy must land before exit
+        return;
+    }
+    if (a.kind == FK_BRANCH) {
+        bocc = meta[2];
+        boff = meta[3];
+        load_chunk(0, min(16, n));
+    }
+    const float g_last = __int_as_float(meta[4]);
+    float acc[2][4][4] = {};   // [mt][nt][fragment]
+#pragma unroll 1
+    for (int kc0 = 0; kc0 < n; kc0 += 16) {
+        const int kn = min(16, n - kc0);
+        if (kc0 > 0) {
+            __syncthreads();   // every warp is done with the previous chunk
+            load_chunk(kc0, kn);
+        }
+        cp_async_wait_all();
+        __syncthreads();
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks) {
+            if (8 * ks >= kn) break;
+            // tokens A = 8 ks + t (k = t), B = A + 4 (k = t + 4); past the
+            // slot's count: zero keys and weights (shared memory holds garbage)
+            const int ia = 8 * ks + t, ib = ia + 4;
+            const bool va = ia < kn, vb = ib < kn;
+            const float wa = va ? expf(g_last - gv[2 * ks]) : 0.f;
+            const float wb = vb ? expf(g_last - gv[2 * ks + 1]) : 0.f;
+            const float4 ua = load4(reinterpret_cast<const UT *>(U_s + ia * UB) + 4 * g);
+            const float4 ub = load4(reinterpret_cast<const UT *>(U_s + ib * UB) + 4 * g);
+            // (rows past the loaded count may hold another CTA's bytes: select, never scale)
+            const float ya[4] = {va ? wa * ua.x : 0.f, va ? wa * ua.y : 0.f, va ? wa * ua.z : 0.f, va ? wa * ua.w : 0.f};
+            const float yb[4] = {vb ? wb * ub.x : 0.f, vb ? wb * ub.y : 0.f, vb ? wb * ub.z : 0.f, vb ? wb * ub.w : 0.f};
+            uint32_t bh0[4], bl0[4], bh1[4], bl1[4];
+#pragma unroll
+            for (int nt = 0; nt < 4; ++nt) {
+                const float ha = tf32_rna(ya[nt]), hb = tf32_rna(yb[nt]);
+                bh0[nt] = __float_as_uint(ha);
+                bl0[nt] = __float_as_uint(ya[nt] - ha);
+                bh1[nt] = __float_as_uint(hb);
+                bl1[nt] = __float_as_uint(yb[nt] - hb);
+            }
+            const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+            const float4 ka = va ? load4(reinterpret_cast<const InT *>(K_s + ia * KB) + c0) : z4;
+            const float4 kb = vb ? load4(reinterpret_cast<const InT *>(K_s + ib * KB) + c0) : z4;
+            const float af[2][4] = {{ka.x, ka.y, kb.x, kb.y}, {ka.z, ka.w, kb.z, kb.w}};
+            uint32_t ah[2][4], al[2][4];
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const float hi = FP32_IN ? tf32_rna(af[mt][e]) : af[mt][e];   // bf16 keys are exact in tf32
+                    ah[mt][e] = __float_as_uint(hi);
+                    al[mt][e] = __float_as_uint(af[mt][e] - hi);
+                }
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+                for (int nt = 0; nt < 4; ++nt) {
+                    mma_tf32_16x8x8(acc[mt][nt], ah[mt], bl0[nt], bl1[nt]);
+                    if (FP32_IN) mma_tf32_16x8x8(acc[mt][nt], al[mt], bh0[nt], bh1[nt]);
+                    mma_tf32_16x8x8(acc[mt][nt], ah[mt], bh0[nt], bh1[nt]);
+                }
+        }
+    }
+    // ---- epilogue: S_new[j][c] = e^{G_last} S0[j][c] + D[c][j]
+    if (!zero_s0) mbar_wait(&bar_ld, 0);
+    const float eG = expf(g_last);
+#pragma unroll
+    for (int p = 0; p < 2; ++p)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) {
+            const int j = 8 * t + 4 * p + nt;
+            float4 v = make_float4(acc[0][nt][p], acc[0][nt][p + 2], acc[1][nt][p], acc[1][nt][p + 2]);
+            if (!zero_s0) {
+                const float4 x = *reinterpret_cast<const float4 *>(S_s + j * kD + c0);
+                v = make_float4(fmaf(eG, x.x, v.x), fmaf(eG, x.y, v.y), fmaf(eG, x.z, v.z), fmaf(eG, x.w, v.w));
+            }
+            __stcs(reinterpret_cast<float4 *>(state_out + j * kD + c0), v);
+        }
+
+    // ---- counters: last CTA of the slot resets the buffer
+    if (tid == 0) {
+        const int nct = gridDim.x * gridDim.y;
+        if (a.kind != FK_FORK && atomicAdd(&a.p.ticket[r], 1) == nct - 1) {
+            a.p.ticket[r] = 0;
+            a.p.occ[r] = 0;
+            if (zero_s0) { a.p.mode[r] = 0; a.p.len[r] = 0; }
+        }
+    }
+}
+
+template <typename InT, typename UT, bool FP32_IN, int MINB>
+static cudaError_t launch_fold_wm(const FoldArgs &a, cudaStream_t s) {
+    const bool pg = a.slots || a.p.btab || a.p.sidx;
+    auto kfn = pg ? fold_wm_kernel<InT, UT, FP32_IN, true, MINB> : fold_wm_kernel<InT, UT, FP32_IN, false, MINB>;
+    cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+    if (e != cudaSuccess) return e;
+    return launch_k(kfn, dim3(kD / 32, a.dm.Hv, a.n), dim3(kFoldThreads), 0, s, a.pdl != 0, a);
+}
+
 template <typename InT, typename UT, bool FP32_IN, int NJ, int KCM>
 static cudaError_t launch_fold_cfg(const FoldArgs &a, cudaStream_t s) {
     const FoldSmem L = fold_smem_layout(FP32_IN, NJ, a.kc);
@@ -321,12 +545,18 @@ static cudaError_t launch_fold_cfg(const FoldArgs &a, cudaStream_t s) {
 
 template <typename InT, typename UT, bool FP32_IN>
 static cudaError_t launch_fold_t(const FoldArgs &a, cudaStream_t s) {
-    // d_v rows per CTA.  Every CTA of a TMEM-allocating kernel costs ~0.5 us
-    // of SM-serialised launch/allocation time on B200 (tools/microbench_tmem.cu:
-    // 3.7 ns per CTA GPU-wide vs 0.64 ns for a plain kernel), so launches where
-    // many CTAs fold little or nothing (commits: zero or few accepted drafts)
-    // take 64-row CTAs (half the CTAs): config-3 commit 164 -> 127 us.  Full
-    // flushes keep 32-row CTAs (more CTAs per SM in flight): 57 vs 62 us.
+    // Flushes and compressions take the warp-MMA form (no TMEM allocation
+    // per CTA): config-2 flush 59.1 -> 57.1 us, config 5 (paged, mixed)
+    // 40.0 -> 36.1 ms per step.  Accepted-draft commits keep the tcgen05 form
+    // with 64-row CTAs: their state request waits for the counters (the host
+    // cannot tell which slots fold), and there the 64-row tcgen05 CTA wins
+    // (config-3 commit 136 vs 145 us; profiles/r2h).  LABUF_FOLD=tc|wm
+    // forces one form (A/B).
+    static const int fold_form = [] {
+        const char *e = getenv("LABUF_FOLD");
+        return !e ? -1 : (e[0] == 't' ? 0 : 1);
+    }();
+    if (fold_form == 1 || (fold_form < 0 && a.kind != FK_COMMIT && a.kind != FK_BRANCH)) return launch_fold_wm<InT, UT, FP32_IN, 7>(a, s);
     const int nj = a.spec ? 32 : 64;
     if (nj == 64) return launch_fold_cfg<InT, UT, FP32_IN, 64, kFoldKCMax>(a, s);
     return launch_fold_cfg<InT, UT, FP32_IN, 32, kFoldKCMax>(a, s);
