@@ -328,7 +328,8 @@ __global__ void __launch_bounds__(kFoldThreads, kFoldNJ == 128 ? 2 : (kFoldNJ ==
 // CTAs; this form drops it.  One 4-warp CTA per (32 d_v rows, V head,
 // slot): the 16 KiB S0 tile streams into shared memory with one bulk copy
 // and the chunk's key rows and u values with cp.async, so the registers hold
-// only the accumulators (8 CTAs per SM, 128 KiB of state in flight per SM).
+// only the accumulators (64 registers: 8 CTAs per SM, 128 KiB of state in
+// flight per SM; 7 with block tables).
 // Warp w owns key columns c in [32 w, 32 w + 32).  The MMA rows (M) are key
 // columns and the columns (N) d_v rows, both permuted so that every
 // thread's accumulators are whole float4 rows of the state: M row g / g + 8
@@ -459,17 +460,6 @@ __global__ void __launch_bounds__(kFoldThreads, MINB) fold_wm_kernel(const FoldA
             const float4 ua = load4(reinterpret_cast<const UT *>(U_s + ia * UB) + 4 * g);
             const float4 ub = load4(reinterpret_cast<const UT *>(U_s + ib * UB) + 4 * g);
             // (rows past the loaded count may hold another CTA's bytes: select, never scale)
-            const float ya[4] = {va ? wa * ua.x : 0.f, va ? wa * ua.y : 0.f, va ? wa * ua.z : 0.f, va ? wa * ua.w : 0.f};
-            const float yb[4] = {vb ? wb * ub.x : 0.f, vb ? wb * ub.y : 0.f, vb ? wb * ub.z : 0.f, vb ? wb * ub.w : 0.f};
-            uint32_t bh0[4], bl0[4], bh1[4], bl1[4];
-#pragma unroll
-            for (int nt = 0; nt < 4; ++nt) {
-                const float ha = tf32_rna(ya[nt]), hb = tf32_rna(yb[nt]);
-                bh0[nt] = __float_as_uint(ha);
-                bl0[nt] = __float_as_uint(ya[nt] - ha);
-                bh1[nt] = __float_as_uint(hb);
-                bl1[nt] = __float_as_uint(yb[nt] - hb);
-            }
             const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
             const float4 ka = va ? load4(reinterpret_cast<const InT *>(K_s + ia * KB) + c0) : z4;
             const float4 kb = vb ? load4(reinterpret_cast<const InT *>(K_s + ib * KB) + c0) : z4;
@@ -483,14 +473,21 @@ __global__ void __launch_bounds__(kFoldThreads, MINB) fold_wm_kernel(const FoldA
                     ah[mt][e] = __float_as_uint(hi);
                     al[mt][e] = __float_as_uint(af[mt][e] - hi);
                 }
+            // d_v row 4 g + nt of tokens A / B: one n-tile at a time (few live registers)
 #pragma unroll
-            for (int mt = 0; mt < 2; ++mt)
+            for (int nt = 0; nt < 4; ++nt) {
+                const float ya = va ? wa * (nt == 0 ? ua.x : nt == 1 ? ua.y : nt == 2 ? ua.z : ua.w) : 0.f;
+                const float yb = vb ? wb * (nt == 0 ? ub.x : nt == 1 ? ub.y : nt == 2 ? ub.z : ub.w) : 0.f;
+                const float ha = tf32_rna(ya), hb = tf32_rna(yb);
+                const uint32_t bh0 = __float_as_uint(ha), bl0 = __float_as_uint(ya - ha);
+                const uint32_t bh1 = __float_as_uint(hb), bl1 = __float_as_uint(yb - hb);
 #pragma unroll
-                for (int nt = 0; nt < 4; ++nt) {
-                    mma_tf32_16x8x8(acc[mt][nt], ah[mt], bl0[nt], bl1[nt]);
-                    if (FP32_IN) mma_tf32_16x8x8(acc[mt][nt], al[mt], bh0[nt], bh1[nt]);
-                    mma_tf32_16x8x8(acc[mt][nt], ah[mt], bh0[nt], bh1[nt]);
+                for (int mt = 0; mt < 2; ++mt) {
+                    mma_tf32_16x8x8(acc[mt][nt], ah[mt], bl0, bl1);
+                    if (FP32_IN) mma_tf32_16x8x8(acc[mt][nt], al[mt], bh0, bh1);
+                    mma_tf32_16x8x8(acc[mt][nt], ah[mt], bh0, bh1);
                 }
+            }
         }
     }
     // ---- epilogue: S_new[j][c] = e^{G_last} S0[j][c] + D[c][j]
@@ -523,7 +520,8 @@ __global__ void __launch_bounds__(kFoldThreads, MINB) fold_wm_kernel(const FoldA
 template <typename InT, typename UT, bool FP32_IN, int MINB>
 static cudaError_t launch_fold_wm(const FoldArgs &a, cudaStream_t s) {
     const bool pg = a.slots || a.p.btab || a.p.sidx;
-    auto kfn = pg ? fold_wm_kernel<InT, UT, FP32_IN, true, MINB> : fold_wm_kernel<InT, UT, FP32_IN, false, MINB>;
+    // (block-table addressing needs a few more registers: one CTA per SM fewer, no spills)
+    auto kfn = pg ? fold_wm_kernel<InT, UT, FP32_IN, true, MINB - 1> : fold_wm_kernel<InT, UT, FP32_IN, false, MINB>;
     cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
     if (e != cudaSuccess) return e;
     return launch_k(kfn, dim3(kD / 32, a.dm.Hv, a.n), dim3(kFoldThreads), 0, s, a.pdl != 0, a);
@@ -556,7 +554,7 @@ static cudaError_t launch_fold_t(const FoldArgs &a, cudaStream_t s) {
         const char *e = getenv("LABUF_FOLD");
         return !e ? -1 : (e[0] == 't' ? 0 : 1);
     }();
-    if (fold_form == 1 || (fold_form < 0 && a.kind != FK_COMMIT && a.kind != FK_BRANCH)) return launch_fold_wm<InT, UT, FP32_IN, 7>(a, s);
+    if (fold_form == 1 || (fold_form < 0 && a.kind != FK_COMMIT && a.kind != FK_BRANCH)) return launch_fold_wm<InT, UT, FP32_IN, 8>(a, s);
     const int nj = a.spec ? 32 : 64;
     if (nj == 64) return launch_fold_cfg<InT, UT, FP32_IN, 64, kFoldKCMax>(a, s);
     return launch_fold_cfg<InT, UT, FP32_IN, 32, kFoldKCMax>(a, s);
