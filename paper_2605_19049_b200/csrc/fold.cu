@@ -548,13 +548,15 @@ static cudaError_t launch_fold_t(const FoldArgs &a, cudaStream_t s) {
     // 40.0 -> 36.1 ms per step.  Accepted-draft commits keep the tcgen05 form
     // with 64-row CTAs: their state request waits for the counters (the host
     // cannot tell which slots fold), and there the 64-row tcgen05 CTA wins
-    // (config-3 commit 136 vs 145 us; profiles/r2h).  LABUF_FOLD=tc|wm
+    // (config-3 commit 136 vs 145 us; profiles/r2h); commits where every
+    // slot holds buffered records (a.spec) take the warp-MMA form too.
+    // LABUF_FOLD=tc|wm
     // forces one form (A/B).
     static const int fold_form = [] {
         const char *e = getenv("LABUF_FOLD");
         return !e ? -1 : (e[0] == 't' ? 0 : 1);
     }();
-    if (fold_form == 1 || (fold_form < 0 && a.kind != FK_COMMIT && a.kind != FK_BRANCH)) return launch_fold_wm<InT, UT, FP32_IN, 8>(a, s);
+    if (fold_form == 1 || (fold_form < 0 && ((a.kind != FK_COMMIT && a.kind != FK_BRANCH) || a.spec))) return launch_fold_wm<InT, UT, FP32_IN, 8>(a, s);
     const int nj = a.spec ? 32 : 64;
     if (nj == 64) return launch_fold_cfg<InT, UT, FP32_IN, 64, kFoldKCMax>(a, s);
     return launch_fold_cfg<InT, UT, FP32_IN, 32, kFoldKCMax>(a, s);

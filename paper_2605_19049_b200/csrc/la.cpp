@@ -769,9 +769,14 @@ la_status la_commit_accepted(la_buf *b, int32_t first, int32_t n, const int32_t 
     if ((st = set_device(b)) != LA_OK) return st;
     FoldArgs a;
     a.dm = b->dm; a.p = b->p; a.first = first; a.n = n;
-    int occ_max = 0;
-    for (int r = first; r < first + n; ++r) occ_max = std::max(occ_max, b->occ[r]);
-    a.kind = FK_COMMIT; a.nacc = n_accepted; a.n_draft = nd; a.kcap = occ_max + nd; a.spec = 0;
+    int occ_max = 0, occ_min = INT32_MAX;
+    for (int r = first; r < first + n; ++r) {
+        occ_max = std::max(occ_max, b->occ[r]);
+        occ_min = std::min(occ_min, b->occ[r]);
+    }
+    // every slot holding buffered records folds (n = occ + n_acc >= 1): the
+    // state tiles can be requested at entry (multi-round speculation)
+    a.kind = FK_COMMIT; a.nacc = n_accepted; a.n_draft = nd; a.kcap = occ_max + nd; a.spec = occ_min > 0;
     std::lock_guard<std::mutex> lk(g_enqueue_mu);
     cudaError_t e = run_fold(b, a, static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(e, "commit launch");
